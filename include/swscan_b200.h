@@ -1,0 +1,135 @@
+/*
+ * swscan_b200.h -- C ABI of the B200-native striped Smith-Waterman library
+ * (libswscan_b200.so).  Plain pointers and sizes only; every device pointer is
+ * caller-owned CUDA memory, every call is asynchronous on `stream`.
+ *
+ * Each entry point replaces one operator of the reference package
+ * (/root/reference/pkg/src/swscan); the reference interface is cited beside it.
+ * Return value: 0 on success, a negative SW_E* code on error (message in
+ * sw_last_error()).  Score overflow is a per-alignment flag, never an error
+ * (reference: src/vectors.py:145-154).
+ *
+ * Scores are exact. End coordinates are the 0-based (ref_end, query_end) of
+ * the first cell reaching the best score in the reference's scalar loop order
+ * (reference residue outer, query position inner; src/_compiled.py:83-114);
+ * (-1, -1) for score 0.  See DESIGN.md "End coordinates".
+ */
+#ifndef SWSCAN_B200_H
+#define SWSCAN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sw_stream_t; /* == cudaStream_t */
+
+enum {
+  SW_OK = 0,
+  SW_EINVAL = -1,   /* bad argument (reference: ValueError / ProfileMismatch) */
+  SW_ECUDA = -2,    /* CUDA launch / runtime failure */
+  SW_ENOTSUP = -3,  /* shape outside the compiled kernel set */
+};
+
+/* kernels: the reference's _KERNEL_IDS {"lazyf": 0, "lazyf-noexit": 1, "scan": 2}
+ * (src/_compiled.py:576) plus the parity-mode lazy-F that mirrors the
+ * reference's E recurrence so per-column pass counts match bit for bit. */
+enum {
+  SW_KERNEL_LAZYF = 0,
+  SW_KERNEL_LAZYF_NOEXIT = 1,
+  SW_KERNEL_SCAN = 2,
+  SW_KERNEL_LAZYF_MIRROR = 3,
+  SW_KERNEL_LAZYF_NOEXIT_MIRROR = 4,
+};
+
+/* per-alignment flag bits */
+enum {
+  SW_FLAG_REF_OVERFLOW = 1, /* reference uint16 kernels would saturate: exact > 65535 - bias */
+  SW_FLAG_RESCUE = 2,       /* 16-bit run hit the wrap guard (internal; cleared by rescue) */
+  SW_FLAG_RESCUED = 4,      /* result comes from the 32-bit re-run */
+};
+
+/* Striped layout chosen for one query (reference: VectorSpec(lanes) +
+ * QueryProfile.seg_len, src/vectors.py:21-36, src/profile.py:26-51). */
+typedef struct sw_plan {
+  int32_t width;      /* score bits: 16 (two lanes per register) or 32 */
+  int32_t lanes;      /* P: stripes per alignment (reference p) */
+  int32_t threads;    /* T: threads per alignment (P/2 for 16-bit, P for 32-bit) */
+  int32_t seg_len;    /* L = ceil(m / P) */
+  int32_t lmax;       /* register words per thread of the kernel instance (>= L) */
+  int32_t m;          /* query length */
+  int32_t n_sym;      /* alphabet size A */
+  int32_t prof_words; /* 32-bit words of the device profile: (A+1) * L * T */
+} sw_plan_t;
+
+int32_t sw_version(void);
+const char* sw_last_error(void);
+
+/* Choose (P, T, L) for a query of length m.  lanes = 0 picks the throughput
+ * layout; lanes = p reproduces the reference layout for VectorSpec(p).
+ * Reference: build_profile_arrays(query, scheme, p), src/_compiled.py:579-585. */
+int32_t sw_plan_query(int32_t m, int32_t n_sym, int32_t width, int32_t lanes, sw_plan_t* out);
+
+/* Build the striped device profile (reference _build_profile_c,
+ * src/_compiled.py:59-73; build_profile src/profile.py:37-72).
+ * d_query: uint8 codes [m]; d_sub: int8 [n_sym][n_sym]; d_prof: prof_words. */
+int32_t sw_profile_build(const sw_plan_t* plan, const uint8_t* d_query, const int8_t* d_sub,
+                         int32_t bias, uint32_t* d_prof, sw_stream_t stream);
+
+/* One prebuilt query profile against n targets (database search form).
+ * Reference: align_prebuilt(kernel, prof, bias, ref, scheme), src/_compiled.py:588-607,
+ * applied to every target.  Targets: d_tgt bytes, target j = d_tgt[d_start[j] ..
+ * d_start[j] + d_len[j]).  d_order (nullable): processing order of job ids
+ * (length-sorted, descending, for load balance).  d_n_jobs (nullable): device
+ * job count overriding n: a rescue pass that runs without a host sync; its
+ * results are marked SW_FLAG_RESCUED.
+ * Outputs are indexed by job id; d_ref_end/d_query_end/d_flags/d_col_passes nullable.
+ * d_col_passes (lazy-F kernels): per-column correction passes of job 0. */
+int32_t sw_db_align(const sw_plan_t* plan, const uint32_t* d_prof, int32_t kernel,
+                    int32_t gap_open, int32_t gap_extend, int32_t bias, int32_t max_sub,
+                    const uint8_t* d_tgt, const int64_t* d_start, const int32_t* d_len,
+                    const int32_t* d_order, int64_t n, const int64_t* d_n_jobs,
+                    int32_t* d_score, int32_t* d_ref_end, int32_t* d_query_end, uint8_t* d_flags,
+                    int32_t* d_col_passes, sw_stream_t stream);
+
+/* n independent (query_k, target_k) pairs.  Reference: batch_align(kernel_id, p,
+ * flat_q, q_off, flat_r, r_off, match_a, mis_a, go_a, ge_a), src/_compiled.py:504-529.
+ * Scoring: a shared d_sub [n_sym][n_sym] with gap_open/gap_extend, or (d_sub NULL)
+ * per-pair 4x4 match/mismatch schemes d_match/d_mismatch/d_go/d_ge like batch_align.
+ * lanes = 0 picks the throughput layout; max_qlen bounds every query length. */
+int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8_t* d_qry,
+                       const int64_t* d_qstart, const int32_t* d_qlen, const uint8_t* d_tgt,
+                       const int64_t* d_tstart, const int32_t* d_tlen, const int32_t* d_order,
+                       int64_t n, const int64_t* d_n_jobs, int32_t max_qlen, const int8_t* d_sub,
+                       int32_t n_sym, int32_t gap_open, int32_t gap_extend, int32_t bias,
+                       int32_t max_sub, const int32_t* d_match, const int32_t* d_mismatch,
+                       const int32_t* d_go, const int32_t* d_ge, int32_t* d_score,
+                       int32_t* d_ref_end, int32_t* d_query_end, uint8_t* d_flags,
+                       int32_t* d_col_passes, sw_stream_t stream);
+
+/* Gather the ids of alignments whose flags intersect `mask` into d_list and
+ * their count into *d_count (device int64).  Used to re-run 16-bit overflow
+ * suspects in 32 bits without a host round trip. */
+int32_t sw_collect_flagged(const uint8_t* d_flags, int64_t n, uint8_t mask, int32_t* d_list,
+                           int64_t* d_count, sw_stream_t stream);
+
+/* Device weighted max-plus scan over P lanes (reference weighted_max_scan /
+ * _weighted_max_scan_c, src/kernels.py:177-201, src/_compiled.py:448-460):
+ * d_f, d_out: uint16 [n][lanes]; d_d: decay per vector.  Values must fit the
+ * signed lane width (< 32768 for width 16). */
+int32_t sw_scan_lanes(int32_t width, int32_t lanes, const uint16_t* d_f, const int32_t* d_d,
+                      int32_t n, uint16_t* d_out, sw_stream_t stream);
+
+/* Diagnostics: launch the DPX issue-rate probe (kind 0: VIADDMNMX.S16x2 only;
+ * kind 1: the cell-update instruction mix) on every SM; returns the number of
+ * per-thread DPX instructions it executes (time it with events on `stream`),
+ * or a negative SW_E* code.  d_scratch: >= 256 words.  Used for the roofline
+ * denominator; no reference counterpart. */
+int64_t sw_dpx_probe(int32_t kind, int64_t iters, uint32_t* d_scratch, sw_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SWSCAN_B200_H */

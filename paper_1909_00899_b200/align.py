@@ -1,0 +1,407 @@
+"""Reference-compatible alignment entry points on the B200 kernels.
+
+Mirrors the reference operator interface (``swscan._compiled`` and the pure
+kernels): ``build_profile_arrays`` / ``align_prebuilt`` / ``align_pair`` /
+``scalar_score`` / ``batch_align`` / ``batch_oracle_scores`` keep their names,
+argument meaning and error behaviour (src/_compiled.py:491-645,
+src/kernels.py:62-264). Differences, all documented in DESIGN.md:
+
+* results carry exact end coordinates ``ref_end`` / ``query_end``;
+* ``score`` is always exact: 16-bit runs that approach the wrap guard are
+  re-run in 32 bits on the device; ``overflow`` keeps the reference meaning
+  (the uint16 reference kernels would saturate, i.e. exact > 65535 - bias);
+* ``p`` selects the reference stripe count when a compiled kernel instance
+  exists for it, otherwise the throughput layout is used (scores and end
+  coordinates do not depend on p; per-column pass counts do).
+
+Device memory and streams come from torch; the compute is the CUDA library
+(``_lib``). There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .scoring import ScoringScheme, SymbolOutOfAlphabet
+
+
+class ProfileMismatch(ValueError):
+    """Profile was built for a different scheme or vector shape (src/kernels.py:27-28)."""
+
+
+class EmptyQuery(ValueError):
+    """Profile construction requires at least one query residue (src/profile.py:18-19)."""
+
+
+@dataclass
+class OpCounters:
+    """Reference vector-op tally (src/vectors.py:61-95), reconstructed in closed
+    form from the device's per-column pass counts."""
+
+    shifts: int = 0
+    sat_adds: int = 0
+    sat_subs: int = 0
+    maxes: int = 0
+    loads: int = 0
+    stores: int = 0
+    correction_passes: int = 0
+
+    @property
+    def vec_ops_total(self) -> int:
+        return self.shifts + self.sat_adds + self.sat_subs + self.maxes + self.loads + self.stores
+
+
+@dataclass
+class AlignmentResult:
+    """src/kernels.py:62-76 plus end coordinates (0-based, -1 when score is 0)."""
+
+    score: int
+    overflow: bool
+    counters: OpCounters | None
+    correction_passes: int
+    column_passes: tuple[int, ...]
+    ref_end: int = -1
+    query_end: int = -1
+    lanes: int = 0
+    seg_len: int = 0
+    rescued: bool = False
+
+
+def scan_steps(p: int) -> int:
+    """_scan_steps, src/_compiled.py:39-46."""
+    s = 0
+    while (1 << s) < p:
+        s += 1
+    return max(1, s)
+
+
+def counters_from_passes(kernel: str, n: int, L: int, p: int, passes: np.ndarray) -> OpCounters:
+    """Closed-form reference counters (src/_compiled.py:137-219, :246-339)."""
+    if kernel == "scan":
+        s = scan_steps(p)
+        return OpCounters(shifts=n * (2 + s), sat_adds=n * L, sat_subs=n * (1 + 5 * L + s),
+                          maxes=n * (1 + 6 * L + s), loads=n * (1 + 3 * L), stores=n * 2 * L,
+                          correction_passes=n * s)
+    k = int(passes.sum())
+    early = kernel.startswith("lazyf") and "noexit" not in kernel
+    broke = int(np.count_nonzero(passes < p)) if early else 0
+    return OpCounters(shifts=n + k + broke, sat_adds=n * L, sat_subs=n * 4 * L + k * L,
+                      maxes=n * 5 * L + k * L, loads=n * (1 + 3 * L) + k * L,
+                      stores=n * 2 * L + k * L, correction_passes=k)
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _to_dev(x, dtype: torch.dtype) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(device="cuda", dtype=dtype).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x))).to(device="cuda", dtype=dtype)
+
+
+def _require_cuda() -> None:
+    _lib.load()
+    if not torch.cuda.is_available():
+        raise _lib.NativeUnavailable("no CUDA device: the B200 kernels have no CPU fallback")
+
+
+def _codes(seq, n_sym: int, what: str) -> np.ndarray:
+    if isinstance(seq, torch.Tensor):
+        arr = seq.detach().cpu().numpy()
+    else:
+        arr = np.asarray(seq)
+    arr = arr.astype(np.int64, copy=False).ravel()
+    if arr.size and (arr.min() < 0 or arr.max() >= n_sym):
+        bad = int(arr[(arr < 0) | (arr >= n_sym)][0])
+        raise SymbolOutOfAlphabet(f"{what} index {bad} outside 0..{n_sym - 1}")
+    return arr.astype(np.uint8)
+
+
+def _kernel_id(kernel: str) -> int:
+    return _lib.KERNEL_IDS[kernel]  # KeyError on unknown names, as the reference
+
+
+@dataclass
+class DeviceProfile:
+    """Striped query profile resident in HBM (reference: the (prof, bias) pair of
+    build_profile_arrays, src/_compiled.py:579-585), 16-bit layout plus the
+    32-bit layout used by overflow rescues."""
+
+    scheme: ScoringScheme
+    m: int
+    query: torch.Tensor
+    sub: torch.Tensor
+    bias: int
+    max_sub: int
+    plan16: _lib.Plan
+    prof16: torch.Tensor
+    requested_lanes: int = 0
+    plan32: _lib.Plan | None = None
+    prof32: torch.Tensor | None = None
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def seg_len(self) -> int:
+        return self.plan16.seg_len
+
+    @property
+    def lanes(self) -> int:
+        return self.plan16.lanes
+
+    def ensure32(self) -> None:
+        if self.plan32 is not None:
+            return
+        lanes = self.requested_lanes if self.requested_lanes and self.requested_lanes <= 32 else 0
+        try:
+            self.plan32 = _lib.plan_query(self.m, self.scheme.n_symbols, 32, lanes)
+        except _lib.SwError:
+            self.plan32 = _lib.plan_query(self.m, self.scheme.n_symbols, 32, 0)
+        self.prof32 = torch.empty(self.plan32.prof_words, dtype=torch.int32, device="cuda")
+        _lib.check(_lib.load().sw_profile_build(C.byref(self.plan32), _ptr(self.query),
+                                                 _ptr(self.sub), self.bias, _ptr(self.prof32),
+                                                 _stream()))
+
+
+def _plan_with_fallback(m: int, n_sym: int, width: int, lanes: int) -> _lib.Plan:
+    if lanes:
+        try:
+            return _lib.plan_query(m, n_sym, width, lanes)
+        except _lib.SwError:
+            pass
+    return _lib.plan_query(m, n_sym, width, 0)
+
+
+def build_profile_arrays(query, scheme: ScoringScheme, p: int = 0) -> DeviceProfile:
+    """Build the striped profile on the device (src/_compiled.py:579-585)."""
+    _require_cuda()
+    q = _codes(query, scheme.n_symbols, "query")
+    if q.size == 0:
+        raise EmptyQuery("query must contain at least one residue")
+    plan = _plan_with_fallback(int(q.size), scheme.n_symbols, 16, int(p))
+    qd = torch.from_numpy(q).cuda()
+    sub = torch.from_numpy(scheme.as_array()).cuda()
+    prof = torch.empty(plan.prof_words, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.load().sw_profile_build(C.byref(plan), _ptr(qd), _ptr(sub), scheme.bias,
+                                             _ptr(prof), _stream()))
+    return DeviceProfile(scheme, int(q.size), qd, sub, scheme.bias, scheme.max_score, plan, prof,
+                         requested_lanes=int(p))
+
+
+def db_align(prof: DeviceProfile, tgt: torch.Tensor, start: torch.Tensor, length: torch.Tensor,
+             order: torch.Tensor | None = None, kernel: str = "scan",
+             col_passes: torch.Tensor | None = None, out: dict | None = None) -> dict:
+    """All-device database alignment: one profile vs n targets, 16-bit with a
+    device-side 32-bit rescue of wrap-guard hits. Returns dict of device tensors
+    ``score, ref_end, query_end, flags`` indexed by target id."""
+    L = _lib.load()
+    n = int(length.shape[0])
+    if out is None:
+        out = {
+            "score": torch.empty(n, dtype=torch.int32, device="cuda"),
+            "ref_end": torch.empty(n, dtype=torch.int32, device="cuda"),
+            "query_end": torch.empty(n, dtype=torch.int32, device="cuda"),
+            "flags": torch.empty(n, dtype=torch.uint8, device="cuda"),
+        }
+    kid = _kernel_id(kernel)
+    sch = prof.scheme
+    st = _stream()
+    _lib.check(L.sw_db_align(C.byref(prof.plan16), _ptr(prof.prof16), kid, sch.gap_open,
+                             sch.gap_extend, prof.bias, prof.max_sub, _ptr(tgt), _ptr(start),
+                             _ptr(length), _ptr(order), n, None, _ptr(out["score"]),
+                             _ptr(out["ref_end"]), _ptr(out["query_end"]), _ptr(out["flags"]),
+                             _ptr(col_passes), st))
+    _rescue_db(prof, tgt, start, length, kid, col_passes, out, n)
+    return out
+
+
+def _rescue_db(prof, tgt, start, length, kid, col_passes, out, n) -> None:
+    L = _lib.load()
+    ws = out.get("_rescue")
+    if ws is None or ws[0].shape[0] < n:
+        ws = (torch.empty(max(n, 1), dtype=torch.int32, device="cuda"),
+              torch.zeros(1, dtype=torch.int64, device="cuda"))
+        out["_rescue"] = ws
+    st = _stream()
+    _lib.check(L.sw_collect_flagged(_ptr(out["flags"]), n, _lib.FLAG_RESCUE, _ptr(ws[0]),
+                                    _ptr(ws[1]), st))
+    prof.ensure32()
+    sch = prof.scheme
+    _lib.check(L.sw_db_align(C.byref(prof.plan32), _ptr(prof.prof32), kid, sch.gap_open,
+                             sch.gap_extend, prof.bias, prof.max_sub, _ptr(tgt), _ptr(start),
+                             _ptr(length), _ptr(ws[0]), 0, _ptr(ws[1]), _ptr(out["score"]),
+                             _ptr(out["ref_end"]), _ptr(out["query_end"]), _ptr(out["flags"]),
+                             _ptr(col_passes), st))
+
+
+def _result_from(prof_or_none, kernel, n, L_, P, score, flags, rend, qend, passes) -> AlignmentResult:
+    fl = int(flags)
+    passes_np = np.asarray(passes, dtype=np.int64) if passes is not None else np.zeros(n, np.int64)
+    if kernel == "scan":
+        passes_np = np.full(n, scan_steps(P), dtype=np.int64)
+    cnt = counters_from_passes(kernel, n, L_, P, passes_np) if n > 0 else OpCounters()
+    return AlignmentResult(score=int(score), overflow=bool(fl & _lib.FLAG_REF_OVERFLOW),
+                           counters=cnt, correction_passes=cnt.correction_passes,
+                           column_passes=tuple(int(x) for x in passes_np), ref_end=int(rend),
+                           query_end=int(qend), lanes=P, seg_len=L_,
+                           rescued=bool(fl & _lib.FLAG_RESCUED))
+
+
+def align_prebuilt(kernel: str, prof: DeviceProfile, bias=None, ref=None,
+                   scheme: ScoringScheme | None = None) -> AlignmentResult:
+    """One alignment against a prebuilt device profile (src/_compiled.py:588-607)."""
+    if not isinstance(prof, DeviceProfile):
+        raise ProfileMismatch("align_prebuilt needs a DeviceProfile from build_profile_arrays")
+    if scheme is not None and (scheme.matrix != prof.scheme.matrix
+                               or scheme.gap_open != prof.scheme.gap_open
+                               or scheme.gap_extend != prof.scheme.gap_extend):
+        raise ProfileMismatch("profile was built for a different scoring scheme")
+    if bias is not None and int(bias) != prof.bias:
+        raise ProfileMismatch("profile was built for a different scoring scheme")
+    kid = _kernel_id(kernel)
+    r = _codes(ref, prof.scheme.n_symbols, "reference")
+    n = int(r.size)
+    if n == 0:
+        return _result_from(None, kernel, 0, prof.seg_len, prof.lanes, 0, 0, -1, -1, None)
+    tgt = torch.from_numpy(r).cuda()
+    start = torch.zeros(1, dtype=torch.int64, device="cuda")
+    length = torch.full((1,), n, dtype=torch.int32, device="cuda")
+    passes = torch.zeros(n, dtype=torch.int32, device="cuda") if kid != 2 else None
+    out = db_align(prof, tgt, start, length, None, kernel, passes)
+    flags = int(out["flags"][0])
+    if flags & _lib.FLAG_RESCUED:
+        P, L_ = prof.plan32.lanes, prof.plan32.seg_len
+    else:
+        P, L_ = prof.lanes, prof.seg_len
+    return _result_from(prof, kernel, n, L_, P, int(out["score"][0]), flags,
+                        int(out["ref_end"][0]), int(out["query_end"][0]),
+                        passes.cpu().numpy() if passes is not None else None)
+
+
+def align_pair(kernel: str, p: int, query, ref, scheme: ScoringScheme) -> AlignmentResult:
+    """src/_compiled.py:610-615."""
+    return align_prebuilt(kernel, build_profile_arrays(query, scheme, p), ref=ref, scheme=scheme)
+
+
+def scalar_score(query, ref, scheme: ScoringScheme) -> int:
+    """Exact local score (src/_compiled.py:618-625), computed by the device kernel."""
+    q = _codes(query, scheme.n_symbols, "query")
+    r = _codes(ref, scheme.n_symbols, "reference")
+    if q.size == 0 or r.size == 0:
+        return 0
+    return align_pair("scan", 0, q, r, scheme).score
+
+
+def pairs_align(flat_q, q_off, flat_r, r_off, *, kernel: str = "scan", lanes: int = 0,
+                scheme: ScoringScheme | None = None, match_a=None, mis_a=None, go_a=None,
+                ge_a=None, width: int = 16) -> dict:
+    """Independent pairs (CSR queries/targets), device-resident results.
+
+    Scoring is either one shared ``scheme`` or per-pair 4x4 match/mismatch
+    schemes like the reference's batch_align (src/_compiled.py:504-529).
+    Returns numpy arrays ``score, ref_end, query_end, flags``."""
+    _require_cuda()
+    L = _lib.load()
+    q_off = np.asarray(q_off, dtype=np.int64)
+    r_off = np.asarray(r_off, dtype=np.int64)
+    n = int(q_off.shape[0] - 1)
+    n_sym = scheme.n_symbols if scheme is not None else 4
+    fq = _codes(flat_q, n_sym, "query")
+    fr = _codes(flat_r, n_sym, "reference")
+    qlen = np.diff(q_off).astype(np.int32)
+    tlen = np.diff(r_off).astype(np.int32)
+    if n == 0:
+        z = np.zeros(0, np.int64)
+        return {"score": z, "ref_end": z.astype(np.int32), "query_end": z.astype(np.int32),
+                "flags": z.astype(np.uint8)}
+    # process pairs grouped by query length (segment length uniform per warp)
+    order = np.lexsort((-tlen, -qlen)).astype(np.int32)
+    dev = {
+        "qry": torch.from_numpy(fq if fq.size else np.zeros(1, np.uint8)).cuda(),
+        "qs": torch.from_numpy(q_off[:-1].copy()).cuda(),
+        "ql": torch.from_numpy(qlen).cuda(),
+        "tgt": torch.from_numpy(fr if fr.size else np.zeros(1, np.uint8)).cuda(),
+        "ts": torch.from_numpy(r_off[:-1].copy()).cuda(),
+        "tl": torch.from_numpy(tlen).cuda(),
+        "order": torch.from_numpy(order).cuda(),
+    }
+    per_pair = scheme is None
+    if per_pair:
+        pp = [torch.from_numpy(np.asarray(x, dtype=np.int32)).cuda()
+              for x in (match_a, mis_a, go_a, ge_a)]
+        sub_t, go, ge, bias, max_sub = None, 0, 0, 0, 0
+    else:
+        pp = [None] * 4
+        sub_t = torch.from_numpy(scheme.as_array()).cuda()
+        go, ge, bias, max_sub = scheme.gap_open, scheme.gap_extend, scheme.bias, scheme.max_score
+    out = {k: torch.empty(n, dtype=torch.int32, device="cuda")
+           for k in ("score", "ref_end", "query_end")}
+    out["flags"] = torch.empty(n, dtype=torch.uint8, device="cuda")
+    max_q = int(qlen.max()) if n else 0
+    kid = _kernel_id(kernel)
+    st = _stream()
+
+    def run(width_, lanes_, order_, n_, n_dev):
+        _lib.check(L.sw_pairs_align(width_, lanes_, kid, _ptr(dev["qry"]), _ptr(dev["qs"]),
+                                    _ptr(dev["ql"]), _ptr(dev["tgt"]), _ptr(dev["ts"]),
+                                    _ptr(dev["tl"]), _ptr(order_), n_, _ptr(n_dev), max_q,
+                                    _ptr(sub_t), n_sym, go, ge, bias, max_sub, *[_ptr(x) for x in pp],
+                                    _ptr(out["score"]), _ptr(out["ref_end"]),
+                                    _ptr(out["query_end"]), _ptr(out["flags"]), None, st))
+
+    lanes_eff = lanes
+    if lanes:
+        try:
+            _lib.plan_query(max_q, n_sym, width, lanes)
+        except _lib.SwError:
+            lanes_eff = 0
+    run(width, lanes_eff, dev["order"], n, None)
+    if width == 16:
+        lst = torch.empty(n, dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        _lib.check(L.sw_collect_flagged(_ptr(out["flags"]), n, _lib.FLAG_RESCUE, _ptr(lst),
+                                        _ptr(cnt), st))
+        l32 = lanes_eff if lanes_eff and lanes_eff <= 32 else 0
+        try:
+            _lib.plan_query(max_q, n_sym, 32, l32)
+        except _lib.SwError:
+            l32 = 0
+        run(32, l32, lst, 0, cnt)
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+def batch_align(kernel_id, p, flat_q, q_off, flat_r, r_off, match_a, mis_a, go_a, ge_a):
+    """src/_compiled.py:504-529: per-pair 4x4 DNA schemes; returns
+    ``(scores int64, overflow uint8, ref_end, query_end)``."""
+    kernel = {0: "lazyf", 1: "lazyf-noexit", 2: "scan"}[int(kernel_id)]
+    r = pairs_align(flat_q, q_off, flat_r, r_off, kernel=kernel, lanes=int(p), match_a=match_a,
+                    mis_a=mis_a, go_a=go_a, ge_a=ge_a)
+    return (r["score"].astype(np.int64), (r["flags"] & _lib.FLAG_REF_OVERFLOW).astype(np.uint8),
+            r["ref_end"], r["query_end"])
+
+
+def batch_oracle_scores(flat_q, q_off, flat_r, r_off, match_a, mis_a, go_a, ge_a):
+    """src/_compiled.py:491-501 (exact scores; here computed by the device scan kernel)."""
+    return batch_align(2, 0, flat_q, q_off, flat_r, r_off, match_a, mis_a, go_a, ge_a)[0]
+
+
+def scan_lanes(f, d, width: int = 32) -> np.ndarray:
+    """Device weighted max-scan over the lanes of each row of ``f`` (weighted_max_scan,
+    src/kernels.py:188-201)."""
+    _require_cuda()
+    f = np.ascontiguousarray(np.atleast_2d(np.asarray(f, dtype=np.uint16)))
+    n, p = f.shape
+    fd = torch.from_numpy(f.view(np.int16)).cuda()
+    dd = torch.from_numpy(np.minimum(np.asarray(d, dtype=np.int64), 2**31 - 1).astype(np.int32)).cuda()
+    out = torch.empty_like(fd)
+    _lib.check(_lib.load().sw_scan_lanes(width, p, _ptr(fd), _ptr(dd), n, _ptr(out), _stream()))
+    return out.cpu().numpy().view(np.uint16)

@@ -1,0 +1,4 @@
+#define SWB_INST_WORD W32
+#define SWB_INST_VAR VAR_LAZYF
+#define SWB_INST_FILL swb_fill_w32_lazyf
+#include "sw_inst.inc"

@@ -1,0 +1,401 @@
+// sw_capi.cu -- extern "C" entry points of libswscan_b200.so (see include/swscan_b200.h).
+//
+// Host-side responsibilities: choose the striped layout, pick the kernel
+// instance from the table, size the persistent grid from the occupancy API,
+// and launch on the caller's stream.  No allocation, no synchronisation.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "sw_kernels.cuh"
+#include "../../include/swscan_b200.h"
+
+using namespace swb;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(SW_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+KernelTable g_tab[2][3];
+std::once_flag g_once;
+
+void init_tables() {
+  std::memset(g_tab, 0, sizeof g_tab);
+  swb_fill_w16_scan(g_tab[0][VAR_SCAN]);
+  swb_fill_w16_lazyf(g_tab[0][VAR_LAZYF]);
+  swb_fill_w16_mirror(g_tab[0][VAR_LAZYF_MIRROR]);
+  swb_fill_w32_scan(g_tab[1][VAR_SCAN]);
+  swb_fill_w32_lazyf(g_tab[1][VAR_LAZYF]);
+  swb_fill_w32_mirror(g_tab[1][VAR_LAZYF_MIRROR]);
+}
+
+int ilog2(int x) {
+  int s = 0;
+  while ((1 << s) < x) ++s;
+  return s;
+}
+
+bool pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+int lmax_index(int L) {
+  for (int i = 0; i < kNumLmax; ++i)
+    if (L <= kLmaxSet[i]) return i;
+  return -1;
+}
+
+// kernel id -> (variant, early_exit)
+bool decode_kernel(int kernel, int* var, int* early_exit) {
+  switch (kernel) {
+    case SW_KERNEL_LAZYF: *var = VAR_LAZYF; *early_exit = 1; return true;
+    case SW_KERNEL_LAZYF_NOEXIT: *var = VAR_LAZYF; *early_exit = 0; return true;
+    case SW_KERNEL_SCAN: *var = VAR_SCAN; *early_exit = 0; return true;
+    case SW_KERNEL_LAZYF_MIRROR: *var = VAR_LAZYF_MIRROR; *early_exit = 1; return true;
+    case SW_KERNEL_LAZYF_NOEXIT_MIRROR: *var = VAR_LAZYF_MIRROR; *early_exit = 0; return true;
+    default: return false;
+  }
+}
+
+// Layout choice.  The throughput layout keeps L near the register budget so
+// the per-column shuffle/scan overhead (~log2 P shuffles) is amortised over
+// many cells; `lanes` > 0 reproduces the reference's VectorSpec(p) exactly.
+int plan(int m, int n_sym, int width, int lanes, sw_plan_t* out) {
+  if (width != 16 && width != 32) return fail(SW_EINVAL, "width must be 16 or 32, got %d", width);
+  if (m < 0) return fail(SW_EINVAL, "query length must be >= 0");
+  if (n_sym < 1 || n_sym > kMaxSym) return fail(SW_ENOTSUP, "alphabet size %d outside 1..%d", n_sym, kMaxSym);
+  const int lpw = width == 16 ? 2 : 1;
+  int P;
+  if (lanes > 0) {
+    if (!pow2(lanes)) return fail(SW_EINVAL, "lanes must be a power of two, got %d", lanes);
+    if (lanes / lpw < (width == 32 ? 2 : 1) || lanes / lpw > 32)
+      return fail(SW_ENOTSUP, "lanes %d outside the warp kernels' range for width %d", lanes, width);
+    P = lanes;
+  } else {
+    // smallest P whose segment fits 32 register words, but at least 16 lanes for
+    // 16-bit (8 threads) so one warp holds 4 alignments in flight.
+    P = width == 16 ? 16 : 8;
+    while ((m + P - 1) / P > 32 && P < 32 * lpw) P *= 2;
+  }
+  const int T = P / lpw;
+  int L = (m + P - 1) / P;
+  if (L < 1) L = 1;
+  const int li = lmax_index(L);
+  if (li < 0)
+    return fail(SW_ENOTSUP, "query length %d needs %d words per lane at %d lanes (max %d)", m, L, P,
+                kLmaxSet[kNumLmax - 1]);
+  out->width = width;
+  out->lanes = P;
+  out->threads = T;
+  out->seg_len = L;
+  out->lmax = kLmaxSet[li];
+  out->m = m;
+  out->n_sym = n_sym;
+  out->prof_words = (n_sym + 1) * L * T;
+  return SW_OK;
+}
+
+int launch(const void* fn, const SwArgs& args, size_t smem, int block, int64_t n_tasks_hint,
+           cudaStream_t stream) {
+  cudaError_t e;
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(smem)");
+  }
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+  if (occ < 1) return fail(SW_ENOTSUP, "kernel does not fit on an SM (smem %zu B)", smem);
+  int64_t grid = (int64_t)sms * occ;
+  const int64_t warps_per_block = block / 32;
+  if (n_tasks_hint > 0) {
+    const int64_t need = (n_tasks_hint + warps_per_block - 1) / warps_per_block;
+    if (need < grid) grid = need;
+  }
+  if (grid < 1) grid = 1;
+  void* params[] = {(void*)&args};
+  e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(block), params, smem, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel(sw_striped_kernel)");
+  return SW_OK;
+}
+
+}  // namespace
+
+namespace swb {
+__global__ void sw_collect_kernel(const uint8_t* __restrict__ flags, int64_t n, uint8_t mask,
+                                  int32_t* __restrict__ list, unsigned long long* __restrict__ count) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool hit = (flags[i] & mask) != 0;
+    const unsigned ballot = __ballot_sync(__activemask(), hit);
+    if (ballot == 0) continue;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(ballot) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(count, (unsigned long long)__popc(ballot));
+    base = __shfl_sync(__activemask(), base, leader);
+    if (hit) list[base + __popc(ballot & ((1u << lane) - 1u))] = (int32_t)i;
+  }
+}
+}  // namespace swb
+
+namespace swb {
+// DPX issue-rate probe: 8 independent dependency chains per thread so the
+// measurement is throughput- (not latency-) bound.  kind 0: VIADDMNMX.S16x2
+// only; kind 1: the cell-update mix of sw_striped_kernel (per word: 2 ADDMNMX.RELU,
+// 2 ADDMNMX, 1 IMNMX, 1 IADD.16x2; 6 instructions).
+__global__ void sw_dpx_probe_kernel(int kind, int64_t iters, uint32_t* out) {
+  uint32_t x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 2654435761u + k;
+  const uint32_t b = 0xfffefffeu, c = 0x00030003u;
+  if (kind == 0) {
+    for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = __viaddmax_s16x2(x[k], b, c);
+    }
+  } else {
+    for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        uint32_t u = __viaddmax_s16x2(x[k], b, x[k + 1]);
+        uint32_t h = __vmaxs2(u, x[k]);
+        uint32_t xu = __vadd2(u, b);
+        x[k + 1] = __viaddmax_s16x2_relu(x[k + 1], c, xu);
+        x[k] = __viaddmax_s16x2_relu(h, b, xu);
+        x[k + 1] = __viaddmax_s16x2(x[k + 1], c, h);
+      }
+    }
+  }
+  uint32_t r = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r ^= x[k];
+  if (r == 0x12345678u) out[threadIdx.x] = r;  // keep the chains live
+}
+}  // namespace swb
+
+extern "C" {
+
+int32_t sw_version(void) { return 1; }
+
+int64_t sw_dpx_probe(int32_t kind, int64_t iters, uint32_t* d_scratch, sw_stream_t stream) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int block = 256, grid = sms * 8;
+  sw_dpx_probe_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(kind, iters, d_scratch);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "sw_dpx_probe_kernel");
+  const int64_t per_iter = kind == 0 ? 8 : 24;  // DPX instructions per thread per iteration
+  return (int64_t)grid * block * iters * per_iter;
+}
+
+const char* sw_last_error(void) { return g_err; }
+
+int32_t sw_plan_query(int32_t m, int32_t n_sym, int32_t width, int32_t lanes, sw_plan_t* out) {
+  if (!out) return fail(SW_EINVAL, "out is NULL");
+  return plan(m, n_sym, width, lanes, out);
+}
+
+int32_t sw_profile_build(const sw_plan_t* p, const uint8_t* d_query, const int8_t* d_sub,
+                         int32_t bias, uint32_t* d_prof, sw_stream_t stream) {
+  if (!p || !d_prof || !d_sub || (p->m > 0 && !d_query)) return fail(SW_EINVAL, "NULL argument");
+  const int words = p->prof_words;
+  const int block = 256;
+  const int grid = (words + block - 1) / block;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int T = p->threads;
+  if (p->width == 16) {
+    switch (T) {
+#define CASE(TT) case TT: sw_profile_kernel<W16, TT><<<grid, block, 0, s>>>(d_query, p->m, d_sub, p->n_sym, p->seg_len, bias, d_prof); break;
+      CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32)
+#undef CASE
+      default: return fail(SW_EINVAL, "bad plan threads %d", T);
+    }
+  } else {
+    switch (T) {
+#define CASE(TT) case TT: sw_profile_kernel<W32, TT><<<grid, block, 0, s>>>(d_query, p->m, d_sub, p->n_sym, p->seg_len, bias, d_prof); break;
+      CASE(2) CASE(4) CASE(8) CASE(16) CASE(32)
+#undef CASE
+      default: return fail(SW_EINVAL, "bad plan threads %d", T);
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SW_OK : cuda_fail(e, "sw_profile_kernel");
+}
+
+int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, int32_t gap_open,
+                    int32_t gap_extend, int32_t bias, int32_t max_sub, const uint8_t* d_tgt,
+                    const int64_t* d_start, const int32_t* d_len, const int32_t* d_order, int64_t n,
+                    const int64_t* d_n_jobs, int32_t* d_score, int32_t* d_ref_end,
+                    int32_t* d_query_end, uint8_t* d_flags, int32_t* d_col_passes,
+                    sw_stream_t stream) {
+  std::call_once(g_once, init_tables);
+  if (!p || !d_prof || !d_tgt || !d_start || !d_len || !d_score)
+    return fail(SW_EINVAL, "NULL argument");
+  if (n < 0) return fail(SW_EINVAL, "n < 0");
+  if (!(gap_open >= gap_extend && gap_extend >= 1))
+    return fail(SW_EINVAL, "require gap_open >= gap_extend >= 1");
+  if (n == 0 && !d_n_jobs) return SW_OK;
+  int var, early;
+  if (!decode_kernel(kernel, &var, &early)) return fail(SW_EINVAL, "unknown kernel %d", kernel);
+  const int wi = p->width == 16 ? 0 : 1;
+  const int li = lmax_index(p->lmax);
+  if (li < 0 || kLmaxSet[li] != p->lmax) return fail(SW_EINVAL, "bad plan lmax %d", p->lmax);
+  const void* fn = g_tab[wi][var][ilog2(p->threads)][li];
+  if (!fn) return fail(SW_ENOTSUP, "no kernel for width %d, threads %d", p->width, p->threads);
+  SwArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.n_jobs = n;
+  a.n_jobs_dev = d_n_jobs;
+  a.order = d_order;
+  a.mode = 0;
+  a.early_exit = early;
+  a.n_sym = p->n_sym;
+  a.shared_L = p->seg_len;
+  a.shared_m = p->m;
+  a.prof = d_prof;
+  a.tgt = d_tgt;
+  a.t_start = d_start;
+  a.t_len = d_len;
+  a.go = gap_open;
+  a.ge = gap_extend;
+  a.bias = bias;
+  a.max_sub = max_sub;
+  a.score = d_score;
+  a.ref_end = d_ref_end;
+  a.query_end = d_query_end;
+  a.flags = d_flags;
+  a.col_passes = d_col_passes;
+  const size_t smem = (size_t)p->prof_words * 4;
+  const int G = 32 / p->threads;
+  const int64_t tasks = d_n_jobs ? 0 : (n + G - 1) / G;
+  return launch(fn, a, smem, 256, tasks, (cudaStream_t)stream);
+}
+
+int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8_t* d_qry,
+                       const int64_t* d_qstart, const int32_t* d_qlen, const uint8_t* d_tgt,
+                       const int64_t* d_tstart, const int32_t* d_tlen, const int32_t* d_order,
+                       int64_t n, const int64_t* d_n_jobs, int32_t max_qlen, const int8_t* d_sub,
+                       int32_t n_sym, int32_t gap_open, int32_t gap_extend, int32_t bias,
+                       int32_t max_sub, const int32_t* d_match, const int32_t* d_mismatch,
+                       const int32_t* d_go, const int32_t* d_ge, int32_t* d_score,
+                       int32_t* d_ref_end, int32_t* d_query_end, uint8_t* d_flags,
+                       int32_t* d_col_passes, sw_stream_t stream) {
+  std::call_once(g_once, init_tables);
+  if (!d_qry || !d_qstart || !d_qlen || !d_tgt || !d_tstart || !d_tlen || !d_score)
+    return fail(SW_EINVAL, "NULL argument");
+  const bool per_pair = d_sub == nullptr;
+  if (per_pair && (!d_match || !d_mismatch || !d_go || !d_ge))
+    return fail(SW_EINVAL, "per-pair schemes need d_match, d_mismatch, d_go and d_ge");
+  if (per_pair) n_sym = 4;
+  if (!per_pair && !(gap_open >= gap_extend && gap_extend >= 1))
+    return fail(SW_EINVAL, "require gap_open >= gap_extend >= 1");
+  if (n < 0) return fail(SW_EINVAL, "n < 0");
+  if (n == 0 && !d_n_jobs) return SW_OK;
+  int var, early;
+  if (!decode_kernel(kernel, &var, &early)) return fail(SW_EINVAL, "unknown kernel %d", kernel);
+  sw_plan_t p;
+  int rc = plan(max_qlen, n_sym, width, lanes, &p);
+  if (rc) return rc;
+  const int wi = width == 16 ? 0 : 1;
+  const void* fn = g_tab[wi][var][ilog2(p.threads)][lmax_index(p.lmax)];
+  if (!fn) return fail(SW_ENOTSUP, "no kernel for width %d, threads %d", width, p.threads);
+  SwArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.n_jobs = n;
+  a.n_jobs_dev = d_n_jobs;
+  a.order = d_order;
+  a.mode = 1;
+  a.early_exit = early;
+  a.n_sym = n_sym;
+  a.tgt = d_tgt;
+  a.t_start = d_tstart;
+  a.t_len = d_tlen;
+  a.qry = d_qry;
+  a.q_start = d_qstart;
+  a.q_len = d_qlen;
+  a.sub = d_sub;
+  a.pp_match = per_pair ? d_match : nullptr;
+  a.pp_mismatch = per_pair ? d_mismatch : nullptr;
+  a.pp_go = per_pair ? d_go : nullptr;
+  a.pp_ge = per_pair ? d_ge : nullptr;
+  a.go = gap_open;
+  a.ge = gap_extend;
+  a.bias = bias;
+  a.max_sub = max_sub;
+  a.score = d_score;
+  a.ref_end = d_ref_end;
+  a.query_end = d_query_end;
+  a.flags = d_flags;
+  a.col_passes = d_col_passes;
+  a.pair_stride = (n_sym + 1) * p.seg_len * p.threads;
+  // block size: as many warps as the per-group profile slices allow (<= 256 threads)
+  int block = 256;
+  const size_t per_thread = (size_t)(n_sym + 1) * p.seg_len * 4;  // slice bytes / T
+  while (block > 32 && per_thread * block > 110 * 1024) block >>= 1;
+  const size_t smem = per_thread * block;
+  if (smem > 227 * 1024) return fail(SW_ENOTSUP, "pair profile slice too large (%zu B)", smem);
+  const int G = 32 / p.threads;
+  const int64_t tasks = d_n_jobs ? 0 : (n + G - 1) / G;
+  return launch(fn, a, smem, block, tasks, (cudaStream_t)stream);
+}
+
+int32_t sw_collect_flagged(const uint8_t* d_flags, int64_t n, uint8_t mask, int32_t* d_list,
+                           int64_t* d_count, sw_stream_t stream) {
+  if (!d_flags || !d_list || !d_count) return fail(SW_EINVAL, "NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(d_count, 0, sizeof(int64_t), s);
+  if (e != cudaSuccess) return cuda_fail(e, "memset count");
+  if (n == 0) return SW_OK;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 4096) blocks = 4096;
+  sw_collect_kernel<<<blocks, 256, 0, s>>>(d_flags, n, mask, d_list, (unsigned long long*)d_count);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? SW_OK : cuda_fail(e, "sw_collect_kernel");
+}
+
+int32_t sw_scan_lanes(int32_t width, int32_t lanes, const uint16_t* d_f, const int32_t* d_d,
+                      int32_t n, uint16_t* d_out, sw_stream_t stream) {
+  if (!d_f || !d_d || !d_out) return fail(SW_EINVAL, "NULL argument");
+  if (n <= 0) return SW_OK;
+  const int lpw = width == 16 ? 2 : (width == 32 ? 1 : 0);
+  if (!lpw || !pow2(lanes)) return fail(SW_EINVAL, "bad width/lanes");
+  const int T = lanes / lpw;
+  if (T < (lpw == 1 ? 2 : 1) || T > 32) return fail(SW_ENOTSUP, "lanes %d unsupported", lanes);
+  const int G = 32 / T;
+  const int warps = (n + G - 1) / G;
+  const int block = 128;
+  const int grid = (warps + 3) / 4;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (lpw == 2) {
+    switch (T) {
+#define CASE(TT) case TT: sw_scan_test_kernel<W16, TT><<<grid, block, 0, s>>>(d_f, d_d, n, d_out); break;
+      CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32)
+#undef CASE
+    }
+  } else {
+    switch (T) {
+#define CASE(TT) case TT: sw_scan_test_kernel<W32, TT><<<grid, block, 0, s>>>(d_f, d_d, n, d_out); break;
+      CASE(2) CASE(4) CASE(8) CASE(16) CASE(32)
+#undef CASE
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SW_OK : cuda_fail(e, "sw_scan_test_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,525 @@
+// sw_kernels.cuh -- B200 (sm_100a) striped Smith-Waterman with the max-plus F scan.
+//
+// One alignment is owned by a *group* of T threads (T = 1..32, a power of two;
+// several groups share a warp).  The query is striped exactly as the reference
+// does it (src/profile.py:37-72, stripe_index :75-81): P virtual lanes, lane l
+// owns query positions [l*L, l*L + L), L = ceil(m / P).  With 16-bit scores a
+// 32-bit register packs two lanes (thread t holds lane t in the low half and
+// lane T+t in the high half, P = 2T) and every cell update is one DPX
+// instruction on both halves; with 32-bit scores P = T.
+//
+// Per reference residue (a "column", src/_compiled.py:247-340) a thread runs
+// its L words serially (the intra-lane F chain is ONE dependent DPX op per
+// word), then the cross-lane F dependency is resolved
+//   * VAR_SCAN  -- by the paper's Alg. 6: a log2(P)-step weighted max-plus scan
+//                  of the column's F (warp shuffles), applied lazily when the
+//                  next column reads H (the deferred correction),
+//   * VAR_LAZYF -- by Farrar's lazy-F loop with the reference's early exit
+//                  (src/_compiled.py:189-217), a group vote per pass.
+// VAR_LAZYF_MIRROR additionally reproduces the reference's E recurrence bit
+// for bit so per-column pass counts equal the reference's (parity mode).
+//
+// Cell update per packed word (F chain = the single dependent op on F):
+//   u  = max(vh + S, E)          diagonal / horizontal gap (E >= 0, so u >= 0)
+//   Hn = max(u, F)               stored H (before cross-lane correction)
+//   Xu = u - go
+//   E  = max(E - ge, Xu, 0)      (MIRROR: max(E - ge, Hn - go, 0))
+//   F  = max(F - ge, Xu, 0)      == reference F' (F - go <= F - ge)
+//   cm = max(cm, u)              column max for score / end coordinates
+//   vh = max(carry - j*ge, Hold) deferred correction (VAR_SCAN)
+// E excludes F-derived H in the fast mode: a vertical->horizontal gap corner
+// costs the same as the horizontal->vertical one the recurrence keeps, so H is
+// exact (the same argument the reference makes for never revisiting E after a
+// correction); the parity tests check it against the oracle.
+//
+// Runtime segment length: words are kept in registers H[0..LMAX), E[0..LMAX);
+// a column enters a fall-through switch at word `first = LMAX - L`, so word c
+// holds segment position j = c - first and the last word is always LMAX-1.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace swb {
+
+enum Variant : int { VAR_SCAN = 0, VAR_LAZYF = 1, VAR_LAZYF_MIRROR = 2 };
+
+// result flag bits (per alignment)
+enum : uint8_t {
+  FLAG_REF_OVERFLOW = 1,  // the reference uint16 kernels would saturate (exact > 65535 - bias)
+  FLAG_RESCUE = 2,        // 16-bit run may have wrapped: re-run in 32 bits
+  FLAG_RESCUED = 4,       // score/coords come from the 32-bit re-run
+};
+
+constexpr int kMaxSym = 32;  // alphabet size limit of the device path (plus one null row)
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// ---- word policies -------------------------------------------------------
+struct W16 {
+  static constexpr int LPW = 2;
+  static constexpr int NULLV = -16384;   // null-residue row (beyond a target's end)
+  static constexpr int CLAMP = 32767;    // decay constants are clamped to the score range
+  __host__ __device__ static constexpr uint32_t splat(int v) {
+    return (uint32_t)(v & 0xffff) * 0x10001u;
+  }
+  __device__ static __forceinline__ uint32_t add(uint32_t a, uint32_t b) { return __vadd2(a, b); }
+  __device__ static __forceinline__ uint32_t vmax(uint32_t a, uint32_t b) { return __vmaxs2(a, b); }
+  __device__ static __forceinline__ uint32_t addmax(uint32_t a, uint32_t b, uint32_t c) {
+    return __viaddmax_s16x2(a, b, c);
+  }
+  __device__ static __forceinline__ uint32_t addmax_relu(uint32_t a, uint32_t b, uint32_t c) {
+    return __viaddmax_s16x2_relu(a, b, c);
+  }
+  __device__ static __forceinline__ int get(uint32_t v, int h) {
+    return h ? (int)(int16_t)(v >> 16) : (int)(int16_t)(v & 0xffffu);
+  }
+  __device__ static __forceinline__ uint32_t pack(int lo, int hi) {
+    return (uint32_t)(lo & 0xffff) | ((uint32_t)hi << 16);
+  }
+  // shift up by K virtual lanes inside a group of T threads: out[l] = v[l-K], 0 for l < K.
+  // `sel` is this thread's PRMT selector for K (identity when t >= K).
+  template <int T, int K>
+  __device__ static __forceinline__ uint32_t shift(uint32_t v, int t, uint32_t gmask, uint32_t sel) {
+    if constexpr (K == T) {
+      return v << 16;
+    } else {
+      uint32_t r = __shfl_sync(gmask, v, (t - K) & (T - 1), T);
+      return prmt(r, 0u, sel);
+    }
+  }
+  __device__ static __forceinline__ uint32_t shift_sel(int t, int k) {
+    return t >= k ? 0x3210u : 0x1044u;  // r<<16: bytes {0,0,r0,r1}
+  }
+};
+
+struct W32 {
+  static constexpr int LPW = 1;
+  static constexpr int NULLV = -(1 << 28);
+  static constexpr int CLAMP = 1 << 29;
+  __host__ __device__ static constexpr uint32_t splat(int v) { return (uint32_t)v; }
+  __device__ static __forceinline__ uint32_t add(uint32_t a, uint32_t b) {
+    return (uint32_t)((int)a + (int)b);
+  }
+  __device__ static __forceinline__ uint32_t vmax(uint32_t a, uint32_t b) {
+    return (uint32_t)max((int)a, (int)b);
+  }
+  __device__ static __forceinline__ uint32_t addmax(uint32_t a, uint32_t b, uint32_t c) {
+    return (uint32_t)__viaddmax_s32((int)a, (int)b, (int)c);
+  }
+  __device__ static __forceinline__ uint32_t addmax_relu(uint32_t a, uint32_t b, uint32_t c) {
+    return (uint32_t)__viaddmax_s32_relu((int)a, (int)b, (int)c);
+  }
+  __device__ static __forceinline__ int get(uint32_t v, int) { return (int)v; }
+  __device__ static __forceinline__ uint32_t pack(int lo, int) { return (uint32_t)lo; }
+  template <int T, int K>
+  __device__ static __forceinline__ uint32_t shift(uint32_t v, int t, uint32_t gmask, uint32_t) {
+    static_assert(K < T, "32-bit lanes shift inside the group");
+    uint32_t r = __shfl_sync(gmask, v, (t - K) & (T - 1), T);
+    return t >= K ? r : 0u;
+  }
+  __device__ static __forceinline__ uint32_t shift_sel(int, int) { return 0u; }
+};
+
+__host__ __device__ constexpr int ceil_log2(int p) {
+  int s = 0;
+  while ((1 << s) < p) ++s;
+  return s == 0 ? 1 : s;  // _scan_steps, src/_compiled.py:39-46
+}
+
+template <class Wd, int T>
+struct Geo {
+  static constexpr int P = T * Wd::LPW;  // virtual lanes per alignment
+  static constexpr int STEPS = ceil_log2(P);
+};
+
+// ---- kernel arguments -----------------------------------------------------
+struct SwArgs {
+  // job description
+  int64_t n_jobs;
+  const int32_t* order;      // job slot -> job id (nullable: identity)
+  int32_t mode;              // 0 = one shared query profile (DB), 1 = per-job query (pairs)
+  int32_t early_exit;        // lazy-F: reference early exit (1) or all P passes (0)
+  int32_t n_sym;             // alphabet size A (profile rows 0..A-1, row A = null residue)
+  int32_t shared_L;          // DB mode: segment length of the shared profile
+  int32_t shared_m;          // DB mode: query length
+  const uint32_t* prof;      // DB mode: global profile [(A+1)][L][T] words
+  // targets (reference sequences)
+  const uint8_t* tgt;
+  const int64_t* t_start;    // [n_jobs] start of job's target in tgt
+  const int32_t* t_len;      // [n_jobs]
+  // queries (pairs mode)
+  const uint8_t* qry;
+  const int64_t* q_start;
+  const int32_t* q_len;
+  // scoring
+  const int8_t* sub;         // pairs mode shared matrix [A][A] (nullable when per-pair 4x4)
+  const int32_t* pp_match;   // pairs mode per-job 4x4 match/mismatch/go/ge (nullable)
+  const int32_t* pp_mismatch;
+  const int32_t* pp_go;
+  const int32_t* pp_ge;
+  int32_t go, ge;            // uniform gaps
+  int32_t bias;              // uniform bias (pairs mode with shared matrix / DB mode)
+  int32_t max_sub;           // uniform max(0, max S)
+  // outputs, indexed by job id
+  int32_t* score;
+  int32_t* ref_end;
+  int32_t* query_end;
+  uint8_t* flags;
+  int32_t* col_passes;       // optional: per-column correction passes (job 0 only)
+  const int64_t* n_jobs_dev; // optional device-side job count (overrides n_jobs; rescue launches)
+  int32_t pair_stride;       // pairs mode: words per group profile slice ((A+1)*Lmax*T)
+};
+
+// ---- the striped kernel -----------------------------------------------------
+#define SWB_REP32(X)                                                                     \
+  X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) \
+  X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29)  \
+  X(30) X(31)
+
+template <class Wd, int T, int LMAX, int VAR>
+__global__ void __launch_bounds__(256)
+sw_striped_kernel(const SwArgs a) {
+  static_assert(LMAX >= 1 && LMAX <= 32, "LMAX");
+  static_assert(T >= 1 && T <= 32 && (T & (T - 1)) == 0, "T");
+  static_assert(Wd::LPW == 2 || T >= 2, "32-bit lanes need T >= 2");
+  constexpr int P = Geo<Wd, T>::P;
+  constexpr int STEPS = Geo<Wd, T>::STEPS;
+  constexpr int G = 32 / T;
+
+  extern __shared__ uint32_t smem[];
+
+  const int lane = threadIdx.x & 31;
+  const int t = lane & (T - 1);
+  const int gw = lane / T;
+  const uint32_t gmask = (T == 32) ? 0xffffffffu : (((1u << T) - 1u) << (gw * T));
+  const int warp_in_block = threadIdx.x >> 5;
+  const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_in_block;
+  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t n_jobs = a.n_jobs_dev ? *a.n_jobs_dev : a.n_jobs;
+  const int64_t n_tasks = (n_jobs + G - 1) / G;
+  const int A = a.n_sym;
+  if ((int64_t)blockIdx.x * (blockDim.x >> 5) >= n_tasks) return;  // nothing for this block
+
+  // shift selectors for K = 1, 2, 4, ... (16-bit packing only)
+  uint32_t sel[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) sel[s] = Wd::shift_sel(t, 1 << s);
+
+  // per-job constants
+  int L = 0, first = 0, m = 0;
+  uint32_t NGO = 0, NGE = 0, NWRAP = 0;
+  uint32_t NJ[LMAX];
+  uint32_t NKD[STEPS];
+  int bias = a.bias, max_sub = a.max_sub;
+
+  auto set_gaps = [&](int go, int ge, int L_) {
+    const int cl = Wd::CLAMP;
+    NGO = Wd::splat(-min(go, cl));
+    NGE = Wd::splat(-min(ge, cl));
+    NWRAP = Wd::splat(-(int)min((int64_t)(L_ - 1) * ge, (int64_t)cl));
+#pragma unroll
+    for (int c = 0; c < LMAX; ++c) {
+      int64_t j = c - (LMAX - L_);
+      NJ[c] = Wd::splat(-(int)min((j < 0 ? 0 : j) * (int64_t)ge, (int64_t)cl));
+    }
+#pragma unroll
+    for (int s = 0; s < STEPS; ++s)
+      NKD[s] = Wd::splat(-(int)min((int64_t)(1 << s) * L_ * (int64_t)ge, (int64_t)cl));
+  };
+
+  const uint32_t* prof_base;  // this thread's profile column (word 0 of row 0)
+  int LT;                     // words per profile row
+  if (a.mode == 0) {
+    // DB mode: one profile for the whole launch, staged in shared memory.
+    L = a.shared_L;
+    m = a.shared_m;
+    first = LMAX - L;
+    LT = L * T;
+    const int words = (A + 1) * LT;
+    const uint4* src = reinterpret_cast<const uint4*>(a.prof);
+    uint4* dst = reinterpret_cast<uint4*>(smem);
+    for (int w = threadIdx.x; w < (words >> 2); w += blockDim.x) dst[w] = __ldg(src + w);
+    for (int w = (words & ~3) + threadIdx.x; w < words; w += blockDim.x) smem[w] = __ldg(a.prof + w);
+    __syncthreads();
+    set_gaps(a.go, a.ge, L);
+    prof_base = smem + t - first * T;
+  } else {
+    LT = 0;
+    prof_base = nullptr;
+  }
+  // pairs mode: each group owns a slice of (A+1)*LMAX*T words
+  uint32_t* gslice = smem + (size_t)((threadIdx.x >> 5) * G + gw) * (size_t)a.pair_stride;
+
+  for (int64_t task = warp_global; task < n_tasks; task += n_warps) {
+    const int64_t slot = task * G + gw;
+    const bool valid = slot < n_jobs;
+    const int64_t job = valid ? (a.order ? (int64_t)a.order[slot] : slot) : 0;
+    const int len = valid ? a.t_len[job] : 0;
+    const uint8_t* tp = a.tgt + (valid ? a.t_start[job] : 0);
+
+    if (a.mode == 1) {
+      // ---- per-job query profile (pairs mode) ----
+      m = valid ? a.q_len[job] : 0;
+      L = (m + P - 1) / P;
+      if (L < 1) L = 1;
+      first = LMAX - L;
+      int go = a.go, ge = a.ge;
+      int mt = 0, mm = 0;
+      const bool pp = a.pp_match != nullptr;
+      if (pp && valid) {
+        mt = a.pp_match[job]; mm = a.pp_mismatch[job]; go = a.pp_go[job]; ge = a.pp_ge[job];
+        bias = max(0, -min(mt, mm));
+        max_sub = max(0, max(mt, mm));
+      }
+      set_gaps(go, ge, L);
+      const uint8_t* qp = a.qry + (valid ? a.q_start[job] : 0);
+      LT = L * T;
+      for (int sym = 0; sym <= A; ++sym) {
+        for (int j = 0; j < L; ++j) {
+          int v[2];
+#pragma unroll
+          for (int h = 0; h < Wd::LPW; ++h) {
+            const int q = (h * T + t) * L + j;
+            int s;
+            if (sym == A) s = Wd::NULLV;
+            else if (q >= m) s = -bias;  // reference pad: profile 0 == -bias (src/profile.py:60-63)
+            else {
+              const int qs = qp[q];
+              s = pp ? (qs == sym ? mt : mm) : (int)a.sub[sym * A + qs];
+            }
+            v[h] = s;
+          }
+          gslice[(sym * L + j) * T + t] = Wd::pack(v[0], v[1]);
+        }
+      }
+      prof_base = gslice + t - first * T;
+    }
+    const int maxlen = __reduce_max_sync(0xffffffffu, len);
+
+    // ---- alignment state ----
+    uint32_t H[LMAX], E[LMAX];
+#pragma unroll
+    for (int c = 0; c < LMAX; ++c) { H[c] = 0u; E[c] = 0u; }
+    uint32_t carry = 0u;
+    uint32_t tb = 0u;  // per-lane best (packed)
+    int bcol[2] = {-1, -1}, bq[2] = {-1, -1};
+    const int nullsym = A;
+    int nxt = (len > 0) ? (int)__ldg(tp) : nullsym;
+
+    for (int i = 0; i < maxlen; ++i) {
+      const int sym = nxt;
+      nxt = (i + 1 < len) ? (int)__ldg(tp + i + 1) : nullsym;
+      const uint32_t* pr = prof_base + sym * LT;
+
+      uint32_t w = H[LMAX - 1];
+      if constexpr (VAR == VAR_SCAN) w = Wd::addmax(carry, NWRAP, w);
+      uint32_t vh = Wd::template shift<T, 1>(w, t, gmask, sel[0]);
+      uint32_t F = 0u, cm = 0u;
+
+#define SWB_WORD(C)                                                        \
+  case C:                                                                  \
+    if constexpr ((C) < LMAX) {                                            \
+      const uint32_t S = pr[(C) * T];                                      \
+      const uint32_t u = Wd::addmax(vh, S, E[C]);                          \
+      const uint32_t Hn = Wd::vmax(u, F);                                  \
+      const uint32_t Xu = Wd::add(u, NGO);                                 \
+      if constexpr (VAR == VAR_LAZYF_MIRROR)                               \
+        E[C] = Wd::addmax_relu(E[C], NGE, Wd::add(Hn, NGO));               \
+      else                                                                 \
+        E[C] = Wd::addmax_relu(E[C], NGE, Xu);                             \
+      F = Wd::addmax_relu(F, NGE, Xu);                                     \
+      cm = Wd::vmax(cm, u);                                                \
+      if constexpr (VAR == VAR_SCAN) vh = Wd::addmax(carry, NJ[C], H[C]);  \
+      else vh = H[C];                                                      \
+      H[C] = Hn;                                                           \
+    }                                                                      \
+    [[fallthrough]];
+
+      switch (first) {
+        SWB_REP32(SWB_WORD)
+        default: break;
+      }
+#undef SWB_WORD
+
+      // ---- end-coordinate bookkeeping (first strict improvement per lane) ----
+      const uint32_t nb = Wd::vmax(tb, cm);
+      if (nb != tb) {
+#pragma unroll
+        for (int h = 0; h < Wd::LPW; ++h) {
+          const int cv = Wd::get(cm, h);
+          if (cv > Wd::get(tb, h)) {
+            int jj = LMAX - 1;
+#pragma unroll
+            for (int c = LMAX - 1; c >= 0; --c)
+              if (c >= first && Wd::get(H[c], h) >= cv) jj = c;
+            bcol[h] = i;
+            bq[h] = (h * T + t) * L + (jj - first);
+          }
+        }
+        tb = nb;
+      }
+
+      // ---- cross-lane F dependency ----
+      if constexpr (VAR == VAR_SCAN) {
+        uint32_t acc = Wd::template shift<T, 1>(F, t, gmask, sel[0]);
+        // Alg. 6 weighted max-scan, k = 1, 2, 4, ... (src/_compiled.py:320-336)
+#define SWB_STEP(S)                                                                         \
+  if constexpr ((S) < STEPS) {                                                             \
+    acc = Wd::addmax_relu(Wd::template shift<T, (1 << (S))>(acc, t, gmask, sel[S]), NKD[S], \
+                          acc);                                                            \
+  }
+        SWB_STEP(0) SWB_STEP(1) SWB_STEP(2) SWB_STEP(3) SWB_STEP(4) SWB_STEP(5)
+#undef SWB_STEP
+        carry = acc;
+      } else {
+        // lazy-F (src/_compiled.py:189-217): shift, optional all-zero exit, correct, repeat
+        uint32_t vf = F;
+        int passes = 0;
+        for (int it = 0; it < P; ++it) {
+          vf = Wd::template shift<T, 1>(vf, t, gmask, sel[0]);
+          if (a.early_exit) {
+            if ((__ballot_sync(gmask, vf != 0u) & gmask) == 0u) break;
+          }
+#define SWB_FIX(C)                                   \
+  case C:                                            \
+    if constexpr ((C) < LMAX) {                      \
+      H[C] = Wd::vmax(H[C], vf);                     \
+      vf = Wd::addmax_relu(vf, NGE, NGE);            \
+    }                                                \
+    [[fallthrough]];
+          switch (first) {
+            SWB_REP32(SWB_FIX)
+            default: break;
+          }
+#undef SWB_FIX
+          ++passes;
+        }
+        if (a.col_passes != nullptr && job == 0 && valid && t == 0 && i < len)
+          a.col_passes[i] = passes;
+      }
+    }
+
+    // ---- reduce (best desc, ref_end asc, query_end asc) over the group ----
+    int best = Wd::get(tb, 0), col = bcol[0], q = bq[0];
+    if constexpr (Wd::LPW == 2) {
+      const int b1 = Wd::get(tb, 1);
+      if (b1 > best || (b1 == best && (bcol[1] < col || (bcol[1] == col && bq[1] < q)))) {
+        best = b1; col = bcol[1]; q = bq[1];
+      }
+    }
+#pragma unroll
+    for (int off = T / 2; off >= 1; off >>= 1) {
+      const int ob = __shfl_xor_sync(gmask, best, off, T);
+      const int oc = __shfl_xor_sync(gmask, col, off, T);
+      const int oq = __shfl_xor_sync(gmask, q, off, T);
+      if (ob > best || (ob == best && (oc < col || (oc == col && oq < q)))) {
+        best = ob; col = oc; q = oq;
+      }
+    }
+    if (valid && t == 0) {
+      uint8_t fl = 0;
+      if constexpr (Wd::LPW == 2) {
+        if (best >= 32767 - max_sub) fl |= FLAG_RESCUE;
+      }
+      if (best > 65535 - bias) fl |= FLAG_REF_OVERFLOW;
+      if (a.n_jobs_dev) fl |= FLAG_RESCUED;  // device-counted launches are rescue passes
+      if (best == 0) { col = -1; q = -1; }
+      a.score[job] = best;
+      if (a.ref_end) a.ref_end[job] = col;
+      if (a.query_end) a.query_end[job] = q;
+      if (a.flags) a.flags[job] = fl;
+    }
+  }
+}
+
+// ---- DB-mode profile builder: prof[(A+1)][L][T] words ------------------------
+// word (a, j, t) packs lanes t and T+t (16-bit) or lane t (32-bit):
+// S[a][query[l*L + j]] for in-range positions, -bias for pads (the reference's
+// profile value 0 minus the bias, src/profile.py:54-64), NULLV for the null row.
+template <class Wd, int T>
+__global__ void sw_profile_kernel(const uint8_t* __restrict__ query, int m, const int8_t* __restrict__ sub,
+                                  int A, int L, int bias, uint32_t* __restrict__ prof) {
+  const int words = (A + 1) * L * T;
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
+    const int t = w % T;
+    const int j = (w / T) % L;
+    const int sym = w / (T * L);
+    int v[2] = {0, 0};
+#pragma unroll
+    for (int h = 0; h < Wd::LPW; ++h) {
+      const int q = (h * T + t) * L + j;
+      if (sym == A) v[h] = Wd::NULLV;
+      else if (q >= m) v[h] = -bias;
+      else v[h] = sub[sym * A + query[q]];
+    }
+    prof[w] = Wd::pack(v[0], v[1]);
+  }
+}
+
+// ---- device weighted max-scan (unit-test entry for the scan device function) ----
+// f: [n][P] uint16 lanes -> out: [n][P], one group of T threads per vector,
+// bit-equal to _weighted_max_scan_c (src/_compiled.py:448-460).
+template <class Wd, int T>
+__global__ void sw_scan_test_kernel(const uint16_t* __restrict__ f, const int32_t* __restrict__ d,
+                                    int n, uint16_t* __restrict__ out) {
+  constexpr int P = Geo<Wd, T>::P;
+  constexpr int STEPS = Geo<Wd, T>::STEPS;
+  constexpr int G = 32 / T;
+  const int lane = threadIdx.x & 31, t = lane & (T - 1), gw = lane / T;
+  const uint32_t gmask = (T == 32) ? 0xffffffffu : (((1u << T) - 1u) << (gw * T));
+  const int vec = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * G + gw;
+  const bool ok = vec < n;
+  const int v = ok ? vec : 0;
+  uint32_t sel[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) sel[s] = Wd::shift_sel(t, 1 << s);
+  // values are uint16 in the reference; the device scan runs on the signed
+  // representation with every decay clamped to the score range.
+  const int lo = f[(size_t)v * P + t];
+  const int hi = (Wd::LPW == 2) ? f[(size_t)v * P + T + t] : 0;
+  uint32_t acc = Wd::pack(lo, hi);
+  acc = Wd::template shift<T, 1>(acc, t, gmask, sel[0]);
+  const int64_t dd = d[v];
+#define SWB_TSTEP(S)                                                                        \
+  if constexpr ((S) < STEPS) {                                                             \
+    const uint32_t nk = Wd::splat(-(int)min((int64_t)(1 << (S)) * dd, (int64_t)Wd::CLAMP)); \
+    acc = Wd::addmax_relu(Wd::template shift<T, (1 << (S))>(acc, t, gmask, sel[S]), nk, acc); \
+  }
+  SWB_TSTEP(0) SWB_TSTEP(1) SWB_TSTEP(2) SWB_TSTEP(3) SWB_TSTEP(4) SWB_TSTEP(5)
+#undef SWB_TSTEP
+  if (ok) {
+    out[(size_t)v * P + t] = (uint16_t)Wd::get(acc, 0);
+    if (Wd::LPW == 2) out[(size_t)v * P + T + t] = (uint16_t)Wd::get(acc, 1);
+  }
+}
+
+}  // namespace swb
+
+namespace swb {
+// gather ids of jobs whose flags intersect `mask` (rescue list)
+__global__ void sw_collect_kernel(const uint8_t* __restrict__ flags, int64_t n, uint8_t mask,
+                                  int32_t* __restrict__ list, unsigned long long* __restrict__ count);
+}  // namespace swb
+
+namespace swb {
+// gather ids of jobs whose flags intersect `mask` (rescue list); count is a device int64
+__global__ void sw_collect_kernel(const uint8_t* __restrict__ flags, int64_t n, uint8_t mask,
+                                  int32_t* __restrict__ list, unsigned long long* __restrict__ count);
+
+// kernel table: [width 0=16,1=32][variant 0..2][log2 T 0..5][lmax idx 0..2]
+constexpr int kNumT = 6;
+constexpr int kNumLmax = 3;
+constexpr int kLmaxSet[kNumLmax] = {8, 16, 32};
+using KernelTable = const void* [kNumT][kNumLmax];
+}  // namespace swb
+
+void swb_fill_w16_scan(swb::KernelTable& t);
+void swb_fill_w16_lazyf(swb::KernelTable& t);
+void swb_fill_w16_mirror(swb::KernelTable& t);
+void swb_fill_w32_scan(swb::KernelTable& t);
+void swb_fill_w32_lazyf(swb::KernelTable& t);
+void swb_fill_w32_mirror(swb::KernelTable& t);

@@ -1,0 +1,193 @@
+"""Database search: one query against a length-binned, sharded target database.
+
+The reference has no database driver; its batch entry point is a serial loop
+over pairs (batch_align, src/_compiled.py:504-529) and the runner aligns one
+pair at a time (src/runner.py:113-159). This module is the B200 replacement for
+that caller side of the hot path:
+
+* ``PackedDb``: the host-side database format -- uint8 residue codes, int64
+  starts, int32 lengths, a length-descending processing order (so the G
+  alignments that share a warp have near-equal length) and global target ids,
+  in pinned memory so uploads run at PCIe/C2C speed;
+* ``shard``: balanced partition of the targets over ranks (round-robin over the
+  length-sorted order, so every rank gets the same cell count to within one
+  target);
+* ``DatabaseSearch``: device buffers + the launch sequence per query (profile
+  build, 16-bit striped kernel, device-side 32-bit rescue, top-k);
+* ``merge_topk``: the cross-rank top-k merge (one all_gather of k records per
+  rank over NCCL -- the only collective of the path).
+
+Top-k order: score descending, then global target id ascending.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .align import DeviceProfile, _ptr, _stream, build_profile_arrays
+from .scoring import ScoringScheme
+
+RECORD_FIELDS = ("score", "target_id", "ref_end", "query_end")
+
+
+@dataclass
+class PackedDb:
+    codes: torch.Tensor  # uint8 [total residues] (pinned host or device)
+    start: torch.Tensor  # int64 [n]
+    length: torch.Tensor  # int32 [n]
+    order: torch.Tensor  # int32 [n] length-descending processing order
+    ids: torch.Tensor  # int64 [n] global target ids
+
+    @property
+    def n(self) -> int:
+        return int(self.length.shape[0])
+
+    @property
+    def residues(self) -> int:
+        return int(self.length.sum())
+
+    def nbytes(self) -> int:
+        return sum(int(t.numel() * t.element_size())
+                   for t in (self.codes, self.start, self.length, self.order, self.ids))
+
+
+def shard(offsets: np.ndarray, rank: int, world: int) -> np.ndarray:
+    """Global target ids owned by `rank`: round-robin over the length-descending order."""
+    lens = np.diff(np.asarray(offsets, dtype=np.int64))
+    by_len = np.argsort(-lens, kind="stable")
+    return np.sort(by_len[rank::world])
+
+
+def pack(db: np.ndarray, offsets: np.ndarray, ids: np.ndarray | None = None,
+         pin: bool = True) -> PackedDb:
+    """Pack the targets `ids` (default: all) of a CSR database into a PackedDb."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    if ids is None:
+        ids = np.arange(offsets.shape[0] - 1, dtype=np.int64)
+    ids = np.asarray(ids, dtype=np.int64)
+    lens = (offsets[ids + 1] - offsets[ids]).astype(np.int64)
+    start = np.zeros(ids.shape[0], dtype=np.int64)
+    if ids.shape[0]:
+        np.cumsum(lens[:-1], out=start[1:])
+    if ids.shape[0] == offsets.shape[0] - 1 and (ids == np.arange(ids.shape[0])).all():
+        codes = np.ascontiguousarray(db[: offsets[-1]], dtype=np.uint8)
+        start = offsets[:-1].copy()
+    else:
+        idx = np.repeat(offsets[ids] - start, lens) + np.arange(int(lens.sum()), dtype=np.int64)
+        codes = np.ascontiguousarray(db[idx], dtype=np.uint8)
+    order = np.argsort(-lens, kind="stable").astype(np.int32)
+
+    def t(a):
+        x = torch.from_numpy(np.ascontiguousarray(a))
+        return x.pin_memory() if pin and torch.cuda.is_available() else x
+
+    return PackedDb(t(codes if codes.size else np.zeros(1, np.uint8)), t(start),
+                    t(lens.astype(np.int32)), t(order), t(ids))
+
+
+class DatabaseSearch:
+    """Device-resident database + per-query launch sequence.
+
+    ``upload(packed)`` copies a PackedDb into device buffers (async on the
+    current stream); ``align(query)`` runs profile build + 16-bit striped kernel
+    + device-side 32-bit rescue; ``topk(k)`` returns the k best records of this
+    rank as a device int64 tensor [k, 4] (score, target_id, ref_end, query_end).
+    """
+
+    def __init__(self, scheme: ScoringScheme, kernel: str = "scan", lanes: int = 0):
+        self.scheme = scheme
+        self.kernel = kernel
+        self.lanes = lanes
+        self.kid = _lib.KERNEL_IDS[kernel]
+        self.dev: PackedDb | None = None
+        self.out: dict | None = None
+        self.prof: DeviceProfile | None = None
+        self.launches = 0
+
+    def upload(self, packed: PackedDb) -> None:
+        n = packed.n
+        if self.dev is None or self.dev.n != n or self.dev.codes.numel() < packed.codes.numel():
+            self.dev = PackedDb(*(torch.empty_like(x, device="cuda") for x in
+                                  (packed.codes, packed.start, packed.length, packed.order,
+                                   packed.ids)))
+            self.out = {
+                "score": torch.empty(n, dtype=torch.int32, device="cuda"),
+                "ref_end": torch.empty(n, dtype=torch.int32, device="cuda"),
+                "query_end": torch.empty(n, dtype=torch.int32, device="cuda"),
+                "flags": torch.empty(n, dtype=torch.uint8, device="cuda"),
+                "_rescue": (torch.empty(max(n, 1), dtype=torch.int32, device="cuda"),
+                            torch.zeros(1, dtype=torch.int64, device="cuda")),
+            }
+        for dst, src in zip((self.dev.codes, self.dev.start, self.dev.length, self.dev.order,
+                             self.dev.ids),
+                            (packed.codes, packed.start, packed.length, packed.order, packed.ids)):
+            dst[: src.numel()].copy_(src, non_blocking=True)
+
+    def set_query(self, query) -> DeviceProfile:
+        self.prof = build_profile_arrays(query, self.scheme, self.lanes)
+        self.prof.ensure32()
+        self.launches += 2
+        return self.prof
+
+    def rebuild_profile(self) -> None:
+        """Re-run the profile kernels for the current query (device-resident)."""
+        L = _lib.load()
+        p = self.prof
+        _lib.check(L.sw_profile_build(C.byref(p.plan16), _ptr(p.query), _ptr(p.sub), p.bias,
+                                      _ptr(p.prof16), _stream()))
+        self.launches += 1
+
+    def align(self) -> dict:
+        assert self.dev is not None and self.prof is not None, "upload() and set_query() first"
+        L = _lib.load()
+        p, d, o, sch = self.prof, self.dev, self.out, self.scheme
+        st = _stream()
+        n = d.n
+        _lib.check(L.sw_db_align(C.byref(p.plan16), _ptr(p.prof16), self.kid, sch.gap_open,
+                                 sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
+                                 _ptr(d.length), _ptr(d.order), n, None, _ptr(o["score"]),
+                                 _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
+                                 None, st))
+        lst, cnt = o["_rescue"]
+        _lib.check(L.sw_collect_flagged(_ptr(o["flags"]), n, _lib.FLAG_RESCUE, _ptr(lst),
+                                        _ptr(cnt), st))
+        _lib.check(L.sw_db_align(C.byref(p.plan32), _ptr(p.prof32), self.kid, sch.gap_open,
+                                 sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
+                                 _ptr(d.length), _ptr(lst), 0, _ptr(cnt), _ptr(o["score"]),
+                                 _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
+                                 None, st))
+        self.launches += 3
+        return o
+
+    def topk(self, k: int = 100) -> torch.Tensor:
+        """k best (score desc, global id asc) as int64 [k, 4] on the device."""
+        o, d = self.out, self.dev
+        k = min(k, d.n)
+        key = (o["score"].to(torch.int64) << 32) | (0xFFFFFFFF - d.ids)
+        _, idx = torch.topk(key, k, sorted=True)
+        return torch.stack([o["score"][idx].to(torch.int64), d.ids[idx],
+                            o["ref_end"][idx].to(torch.int64), o["query_end"][idx].to(torch.int64)],
+                           dim=1)
+
+
+def merge_topk(records: torch.Tensor, k: int, group=None) -> torch.Tensor:
+    """Cross-rank top-k: all_gather k records per rank (NCCL), re-select on every rank."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return records
+    world = dist.get_world_size(group)
+    kk = torch.full((k, 4), -1, dtype=torch.int64, device=records.device)
+    kk[: records.shape[0]] = records
+    kk[records.shape[0]:, 0] = -1  # padding (scores are >= 0) loses every comparison
+    gathered = [torch.empty_like(kk) for _ in range(world)]
+    dist.all_gather(gathered, kk, group=group)
+    allr = torch.cat(gathered)
+    key = (allr[:, 0] << 32) | (0xFFFFFFFF - (allr[:, 1] & 0xFFFFFFFF))
+    _, idx = torch.topk(key, min(k, allr.shape[0]), sorted=True)
+    return allr[idx]

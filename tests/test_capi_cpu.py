@@ -1,0 +1,107 @@
+"""CPU-side checks of the C ABI library and the host layer (no GPU needed)."""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols() -> list[str]:
+    with open(os.path.join(REPO, "include", "swscan_b200.h")) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"^\s*(?:int32_t|int64_t|const char\*)\s+(sw_\w+)\(", text, re.M)))
+
+
+def test_header_declares_the_exported_api():
+    from paper_1909_00899_b200 import _lib
+
+    assert set(_declared_symbols()) == set(_lib.EXPORTS)
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    from paper_1909_00899_b200 import _lib
+
+    _lib.build()
+    lib = C.CDLL(_lib.LIB_PATH)
+    for name in _declared_symbols():
+        assert hasattr(lib, name), name
+    L = _lib.load()
+    assert L.sw_version() == 1
+
+
+def test_plan_reproduces_reference_layout():
+    from paper_1909_00899_b200 import _lib
+
+    _lib.build()
+    for m in (1, 3, 17, 150, 255, 464):
+        for p in (2, 4, 8, 16, 32, 64):
+            L = (m + p - 1) // p
+            if L > 32:
+                with pytest.raises(_lib.SwError):
+                    _lib.plan_query(m, 4, 16, p)
+                continue
+            pl = _lib.plan_query(m, 4, 16, p)
+            assert (pl.lanes, pl.threads, pl.seg_len) == (p, p // 2, L)
+            assert pl.lmax >= L and pl.prof_words == 5 * L * (p // 2)
+    auto = _lib.plan_query(464, 20, 16, 0)
+    assert (auto.lanes, auto.seg_len) == (16, 29)
+    with pytest.raises(_lib.SwError):
+        _lib.plan_query(10, 4, 24, 0)
+    with pytest.raises(_lib.SwError):
+        _lib.plan_query(10, 4, 16, 6)
+
+
+def test_counters_closed_form_matches_reference_tallies(oracle):
+    """Host reconstruction of the reference's op counters from pass counts."""
+    from paper_1909_00899_b200.align import counters_from_passes
+
+    rng = np.random.default_rng(3)
+    sub = np.full((4, 4), -2, np.int8)
+    np.fill_diagonal(sub, 3)
+    for _ in range(30):
+        q = rng.integers(0, 4, int(rng.integers(1, 80)))
+        r = rng.integers(0, 4, int(rng.integers(1, 80)))
+        p = int(rng.choice([2, 4, 8, 16]))
+        for kern in ("scan", "lazyf", "lazyf-noexit"):
+            _, _, cnt, colp = oracle.align_pair(kern, p, q, r, sub, 4, 1)
+            L = (len(q) + p - 1) // p
+            c = counters_from_passes(kern, len(r), L, p, colp)
+            assert [c.shifts, c.sat_adds, c.sat_subs, c.maxes, c.loads, c.stores,
+                    c.correction_passes] == list(cnt)
+
+
+def test_scoring_mirrors_reference_validation():
+    from paper_1909_00899_b200.scoring import Alphabet, ScoringScheme, SymbolOutOfAlphabet
+
+    with pytest.raises(ValueError):
+        ScoringScheme(((1, 2), (3,)), 3, 1)
+    with pytest.raises(ValueError):
+        ScoringScheme(((200,),), 3, 1)
+    with pytest.raises(ValueError):
+        ScoringScheme(((1,),), 1, 2)
+    dna = Alphabet.dna()
+    sch = ScoringScheme.match_mismatch(dna, 2, -3, 5, 2)
+    assert sch.bias == 3 and sch.max_score == 2
+    assert sch.matrix[4] == (-3,) * 5  # wildcard row scores mismatch
+    assert list(dna.encode_array("ACGTN")) == [0, 1, 2, 3, 4]
+    with pytest.raises(SymbolOutOfAlphabet):
+        dna.encode_array("ACGX")
+
+
+def test_product_path_has_no_cpu_fallback(monkeypatch):
+    """Without a CUDA device the product raises instead of computing on the CPU."""
+    import torch
+
+    from paper_1909_00899_b200 import _lib, align
+    from paper_1909_00899_b200.scoring import Alphabet, ScoringScheme
+
+    monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
+    sch = ScoringScheme.match_mismatch(Alphabet("ACGT"), 2, -1, 3, 1)
+    with pytest.raises(_lib.NativeUnavailable):
+        align.align_pair("scan", 8, [0, 1, 2], [0, 1], sch)
