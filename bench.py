@@ -273,6 +273,11 @@ def main() -> None:
     e1.record(stream)
     torch.cuda.synchronize()
     dpx_instr_per_s = n_instr / (e0.elapsed_time(e1) * 1e-3)
+    e0.record(stream)
+    n0 = L.sw_dpx_probe(0, iters, _ptr(scratch), _stream())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    viaddmnmx_per_s = n0 / (e0.elapsed_time(e1) * 1e-3)
     # algorithmic minimum: 6 lane-instructions per cell, 2 cells per 16x2 instruction
     peak_gcups = dpx_instr_per_s * 2 / 6 / 1e9
 
@@ -326,6 +331,8 @@ def main() -> None:
                          "kernel": f"sw_striped_kernel<W16,{p.plan16.threads},{p.plan16.lmax},SCAN>",
                          "kernel_ms": round(k_ms, 3),
                          "peak_source": "live DPX probe (cell-update mix, 6 instr per 2 cells)",
+                         "dpx_probe": {"mix_instr_per_s": dpx_instr_per_s,
+                                       "viaddmnmx_s16x2_instr_per_s": viaddmnmx_per_s},
                          "hbm": {"achieved": round(hbm_achieved, 2), "peak": hbm_peak,
                                  "unit": "GB/s", "frac": round(hbm_achieved / hbm_peak, 5),
                                  "algorithmic_bytes": int(alg_bytes)}},

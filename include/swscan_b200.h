@@ -97,11 +97,13 @@ int32_t sw_db_align(const sw_plan_t* plan, const uint32_t* d_prof, int32_t kerne
  * flat_q, q_off, flat_r, r_off, match_a, mis_a, go_a, ge_a), src/_compiled.py:504-529.
  * Scoring: a shared d_sub [n_sym][n_sym] with gap_open/gap_extend, or (d_sub NULL)
  * per-pair 4x4 match/mismatch schemes d_match/d_mismatch/d_go/d_ge like batch_align.
- * lanes = 0 picks the throughput layout; max_qlen bounds every query length. */
+ * lanes = 0 picks the throughput layout; min_qlen/max_qlen bound the query lengths
+ * (min_qlen = 0 if unknown; equal segment lengths select the exact-length kernels). */
 int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8_t* d_qry,
                        const int64_t* d_qstart, const int32_t* d_qlen, const uint8_t* d_tgt,
                        const int64_t* d_tstart, const int32_t* d_tlen, const int32_t* d_order,
-                       int64_t n, const int64_t* d_n_jobs, int32_t max_qlen, const int8_t* d_sub,
+                       int64_t n, const int64_t* d_n_jobs, int32_t min_qlen, int32_t max_qlen,
+                       const int8_t* d_sub,
                        int32_t n_sym, int32_t gap_open, int32_t gap_extend, int32_t bias,
                        int32_t max_sub, const int32_t* d_match, const int32_t* d_mismatch,
                        const int32_t* d_go, const int32_t* d_ge, int32_t* d_score,

@@ -347,13 +347,14 @@ def pairs_align(flat_q, q_off, flat_r, r_off, *, kernel: str = "scan", lanes: in
            for k in ("score", "ref_end", "query_end")}
     out["flags"] = torch.empty(n, dtype=torch.uint8, device="cuda")
     max_q = int(qlen.max()) if n else 0
+    min_q = int(qlen.min()) if n else 0
     kid = _kernel_id(kernel)
     st = _stream()
 
     def run(width_, lanes_, order_, n_, n_dev):
         _lib.check(L.sw_pairs_align(width_, lanes_, kid, _ptr(dev["qry"]), _ptr(dev["qs"]),
                                     _ptr(dev["ql"]), _ptr(dev["tgt"]), _ptr(dev["ts"]),
-                                    _ptr(dev["tl"]), _ptr(order_), n_, _ptr(n_dev), max_q,
+                                    _ptr(dev["tl"]), _ptr(order_), n_, _ptr(n_dev), min_q, max_q,
                                     _ptr(sub_t), n_sym, go, ge, bias, max_sub, *[_ptr(x) for x in pp],
                                     _ptr(out["score"]), _ptr(out["ref_end"]),
                                     _ptr(out["query_end"]), _ptr(out["flags"]), None, st))

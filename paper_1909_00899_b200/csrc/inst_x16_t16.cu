@@ -1,0 +1,5 @@
+#define SWB_X_T 16
+#define SWB_X_LO 17
+#define SWB_X_HI 32
+#define SWB_X_FILL swb_fill_exact_t16
+#include "sw_inst_exact.inc"

@@ -30,10 +30,16 @@ int cuda_fail(cudaError_t e, const char* what) {
 }
 
 KernelTable g_tab[2][3];
+ExactTable g_exact;  // 16-bit scan, exact segment length
 std::once_flag g_once;
 
 void init_tables() {
   std::memset(g_tab, 0, sizeof g_tab);
+  std::memset(g_exact, 0, sizeof g_exact);
+  swb_fill_exact_t8a(g_exact);
+  swb_fill_exact_t8b(g_exact);
+  swb_fill_exact_t16(g_exact);
+  swb_fill_exact_t32(g_exact);
   swb_fill_w16_scan(g_tab[0][VAR_SCAN]);
   swb_fill_w16_lazyf(g_tab[0][VAR_LAZYF]);
   swb_fill_w16_mirror(g_tab[0][VAR_LAZYF_MIRROR]);
@@ -255,7 +261,9 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
   const int wi = p->width == 16 ? 0 : 1;
   const int li = lmax_index(p->lmax);
   if (li < 0 || kLmaxSet[li] != p->lmax) return fail(SW_EINVAL, "bad plan lmax %d", p->lmax);
-  const void* fn = g_tab[wi][var][ilog2(p->threads)][li];
+  const void* fn = nullptr;
+  if (wi == 0 && var == VAR_SCAN) fn = g_exact[ilog2(p->threads)][p->seg_len];
+  if (!fn) fn = g_tab[wi][var][ilog2(p->threads)][li];
   if (!fn) return fail(SW_ENOTSUP, "no kernel for width %d, threads %d", p->width, p->threads);
   SwArgs a;
   std::memset(&a, 0, sizeof a);
@@ -289,7 +297,8 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
 int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8_t* d_qry,
                        const int64_t* d_qstart, const int32_t* d_qlen, const uint8_t* d_tgt,
                        const int64_t* d_tstart, const int32_t* d_tlen, const int32_t* d_order,
-                       int64_t n, const int64_t* d_n_jobs, int32_t max_qlen, const int8_t* d_sub,
+                       int64_t n, const int64_t* d_n_jobs, int32_t min_qlen, int32_t max_qlen,
+                       const int8_t* d_sub,
                        int32_t n_sym, int32_t gap_open, int32_t gap_extend, int32_t bias,
                        int32_t max_sub, const int32_t* d_match, const int32_t* d_mismatch,
                        const int32_t* d_go, const int32_t* d_ge, int32_t* d_score,
@@ -312,7 +321,11 @@ int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8
   int rc = plan(max_qlen, n_sym, width, lanes, &p);
   if (rc) return rc;
   const int wi = width == 16 ? 0 : 1;
-  const void* fn = g_tab[wi][var][ilog2(p.threads)][lmax_index(p.lmax)];
+  const void* fn = nullptr;
+  // every query of the batch has the same segment length: exact-L instance
+  const bool uniform_L = min_qlen > 0 && (min_qlen + p.lanes - 1) / p.lanes == p.seg_len;
+  if (wi == 0 && var == VAR_SCAN && uniform_L) fn = g_exact[ilog2(p.threads)][p.seg_len];
+  if (!fn) fn = g_tab[wi][var][ilog2(p.threads)][lmax_index(p.lmax)];
   if (!fn) return fail(SW_ENOTSUP, "no kernel for width %d, threads %d", width, p.threads);
   SwArgs a;
   std::memset(&a, 0, sizeof a);

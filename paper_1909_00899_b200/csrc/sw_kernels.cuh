@@ -180,9 +180,11 @@ struct SwArgs {
   X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29)  \
   X(30) X(31)
 
-template <class Wd, int T, int LMAX, int VAR>
+template <class Wd, int T, int LMAX, int VAR, bool EXACT = false>
 __global__ void __launch_bounds__(256)
 sw_striped_kernel(const SwArgs a) {
+  // EXACT: LMAX is the segment length itself (uniform-L launches); the word
+  // loop is straight-line code the scheduler can software-pipeline.
   static_assert(LMAX >= 1 && LMAX <= 32, "LMAX");
   static_assert(T >= 1 && T <= 32 && (T & (T - 1)) == 0, "T");
   static_assert(Wd::LPW == 2 || T >= 2, "32-bit lanes need T >= 2");
@@ -320,30 +322,38 @@ sw_striped_kernel(const SwArgs a) {
       uint32_t vh = Wd::template shift<T, 1>(w, t, gmask, sel[0]);
       uint32_t F = 0u, cm = 0u;
 
+#define SWB_WORD_BODY(C)                                                   \
+  {                                                                        \
+    const uint32_t S = pr[(C) * T];                                        \
+    const uint32_t u = Wd::addmax(vh, S, E[C]);                            \
+    const uint32_t Hn = Wd::vmax(u, F);                                    \
+    const uint32_t Xu = Wd::add(u, NGO);                                   \
+    if constexpr (VAR == VAR_LAZYF_MIRROR)                                 \
+      E[C] = Wd::addmax_relu(E[C], NGE, Wd::add(Hn, NGO));                 \
+    else                                                                   \
+      E[C] = Wd::addmax_relu(E[C], NGE, Xu);                               \
+    F = Wd::addmax_relu(F, NGE, Xu);                                       \
+    cm = Wd::vmax(cm, u);                                                  \
+    if constexpr (VAR == VAR_SCAN) vh = Wd::addmax(carry, NJ[C], H[C]);    \
+    else vh = H[C];                                                        \
+    H[C] = Hn;                                                             \
+  }
 #define SWB_WORD(C)                                                        \
   case C:                                                                  \
-    if constexpr ((C) < LMAX) {                                            \
-      const uint32_t S = pr[(C) * T];                                      \
-      const uint32_t u = Wd::addmax(vh, S, E[C]);                          \
-      const uint32_t Hn = Wd::vmax(u, F);                                  \
-      const uint32_t Xu = Wd::add(u, NGO);                                 \
-      if constexpr (VAR == VAR_LAZYF_MIRROR)                               \
-        E[C] = Wd::addmax_relu(E[C], NGE, Wd::add(Hn, NGO));               \
-      else                                                                 \
-        E[C] = Wd::addmax_relu(E[C], NGE, Xu);                             \
-      F = Wd::addmax_relu(F, NGE, Xu);                                     \
-      cm = Wd::vmax(cm, u);                                                \
-      if constexpr (VAR == VAR_SCAN) vh = Wd::addmax(carry, NJ[C], H[C]);  \
-      else vh = H[C];                                                      \
-      H[C] = Hn;                                                           \
-    }                                                                      \
+    if constexpr ((C) < LMAX) SWB_WORD_BODY(C)                             \
     [[fallthrough]];
 
-      switch (first) {
-        SWB_REP32(SWB_WORD)
-        default: break;
+      if constexpr (EXACT) {
+#pragma unroll
+        for (int c = 0; c < LMAX; ++c) SWB_WORD_BODY(c)
+      } else {
+        switch (first) {
+          SWB_REP32(SWB_WORD)
+          default: break;
+        }
       }
 #undef SWB_WORD
+#undef SWB_WORD_BODY
 
       // ---- end-coordinate bookkeeping (first strict improvement per lane) ----
       const uint32_t nb = Wd::vmax(tb, cm);
@@ -384,18 +394,26 @@ sw_striped_kernel(const SwArgs a) {
           if (a.early_exit) {
             if ((__ballot_sync(gmask, vf != 0u) & gmask) == 0u) break;
           }
-#define SWB_FIX(C)                                   \
-  case C:                                            \
-    if constexpr ((C) < LMAX) {                      \
-      H[C] = Wd::vmax(H[C], vf);                     \
-      vf = Wd::addmax_relu(vf, NGE, NGE);            \
-    }                                                \
+#define SWB_FIX_BODY(C)                      \
+  {                                          \
+    H[C] = Wd::vmax(H[C], vf);               \
+    vf = Wd::addmax_relu(vf, NGE, NGE);      \
+  }
+#define SWB_FIX(C)                           \
+  case C:                                    \
+    if constexpr ((C) < LMAX) SWB_FIX_BODY(C) \
     [[fallthrough]];
-          switch (first) {
-            SWB_REP32(SWB_FIX)
-            default: break;
+          if constexpr (EXACT) {
+#pragma unroll
+            for (int c = 0; c < LMAX; ++c) SWB_FIX_BODY(c)
+          } else {
+            switch (first) {
+              SWB_REP32(SWB_FIX)
+              default: break;
+            }
           }
 #undef SWB_FIX
+#undef SWB_FIX_BODY
           ++passes;
         }
         if (a.col_passes != nullptr && job == 0 && valid && t == 0 && i < len)
@@ -523,3 +541,12 @@ void swb_fill_w16_mirror(swb::KernelTable& t);
 void swb_fill_w32_scan(swb::KernelTable& t);
 void swb_fill_w32_lazyf(swb::KernelTable& t);
 void swb_fill_w32_mirror(swb::KernelTable& t);
+
+// exact-L instances (uniform segment length): [log2 T][L]
+namespace swb {
+using ExactTable = const void* [kNumT][33];
+}
+void swb_fill_exact_t8a(swb::ExactTable& t);
+void swb_fill_exact_t8b(swb::ExactTable& t);
+void swb_fill_exact_t16(swb::ExactTable& t);
+void swb_fill_exact_t32(swb::ExactTable& t);
