@@ -110,6 +110,21 @@ int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8
                        int32_t* d_ref_end, int32_t* d_query_end, uint8_t* d_flags,
                        int32_t* d_col_passes, sw_stream_t stream);
 
+/* Long single pairs (query beyond the warp kernels' 2048 16-bit / 1024 32-bit
+ * positions, e.g. config 4/5): a pipeline of query strips, one warp-sized CTA
+ * per strip, streaming every reference column and passing the strip boundary
+ * (F out, corrected last H) to the next strip through an L2 ring buffer.
+ * Reference: align_pair("scan", p, query, ref, scheme), src/_compiled.py:610-615,
+ * for a single pair.  Scan kernel only.  Outputs are single values (device).
+ * d_workspace: sw_long_workspace_bytes(m, n, n_sym, width) bytes of device memory. */
+int64_t sw_long_workspace_bytes(int64_t m, int64_t n, int32_t n_sym, int32_t width);
+int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int64_t m,
+                      const uint8_t* d_ref, int64_t n, const int8_t* d_sub, int32_t n_sym,
+                      int32_t gap_open, int32_t gap_extend, int32_t bias, int32_t max_sub,
+                      void* d_workspace, int64_t workspace_bytes, int32_t* d_score,
+                      int32_t* d_ref_end, int32_t* d_query_end, uint8_t* d_flags,
+                      sw_stream_t stream);
+
 /* Gather the ids of alignments whose flags intersect `mask` into d_list and
  * their count into *d_count (device int64).  Used to re-run 16-bit overflow
  * suspects in 32 bits without a host round trip. */

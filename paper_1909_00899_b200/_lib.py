@@ -34,6 +34,8 @@ EXPORTS = (
     "sw_collect_flagged",
     "sw_scan_lanes",
     "sw_dpx_probe",
+    "sw_long_workspace_bytes",
+    "sw_align_long",
 )
 
 
@@ -112,6 +114,11 @@ def load():
     L.sw_scan_lanes.argtypes = [i32, i32, vp, vp, i32, vp, vp]
     L.sw_dpx_probe.restype = i64
     L.sw_dpx_probe.argtypes = [i32, i64, vp, vp]
+    L.sw_long_workspace_bytes.restype = i64
+    L.sw_long_workspace_bytes.argtypes = [i64, i64, i32, i32]
+    L.sw_align_long.restype = i32
+    L.sw_align_long.argtypes = [i32, i32, vp, i64, vp, i64, vp, i32, i32, i32, i32, i32, vp, i64,
+                                vp, vp, vp, vp, vp]
     _lib = L
     return L
 

@@ -165,7 +165,7 @@ class DeviceProfile:
         try:
             self.plan32 = _lib.plan_query(self.m, self.scheme.n_symbols, 32, lanes)
         except _lib.SwError:
-            self.plan32 = _lib.plan_query(self.m, self.scheme.n_symbols, 32, 0)
+            self.plan32 = _lib.plan_query(self.m, self.scheme.n_symbols, 32, 0)  # may raise
         self.prof32 = torch.empty(self.plan32.prof_words, dtype=torch.int32, device="cuda")
         _lib.check(_lib.load().sw_profile_build(C.byref(self.plan32), _ptr(self.query),
                                                  _ptr(self.sub), self.bias, _ptr(self.prof32),
@@ -187,9 +187,14 @@ def build_profile_arrays(query, scheme: ScoringScheme, p: int = 0) -> DeviceProf
     q = _codes(query, scheme.n_symbols, "query")
     if q.size == 0:
         raise EmptyQuery("query must contain at least one residue")
-    plan = _plan_with_fallback(int(q.size), scheme.n_symbols, 16, int(p))
     qd = torch.from_numpy(q).cuda()
     sub = torch.from_numpy(scheme.as_array()).cuda()
+    try:
+        plan = _plan_with_fallback(int(q.size), scheme.n_symbols, 16, int(p))
+    except _lib.SwError:
+        # longer than the warp kernels hold: the strip pipeline (align_long) runs it
+        return DeviceProfile(scheme, int(q.size), qd, sub, scheme.bias, scheme.max_score, None,
+                             None, requested_lanes=int(p))
     prof = torch.empty(plan.prof_words, dtype=torch.int32, device="cuda")
     _lib.check(_lib.load().sw_profile_build(C.byref(plan), _ptr(qd), _ptr(sub), scheme.bias,
                                              _ptr(prof), _stream()))
@@ -197,9 +202,46 @@ def build_profile_arrays(query, scheme: ScoringScheme, p: int = 0) -> DeviceProf
                          requested_lanes=int(p))
 
 
+def align_long(query, ref, scheme: ScoringScheme, width: int = 32, kernel: str = "scan",
+               query_dev: torch.Tensor | None = None, ref_dev: torch.Tensor | None = None) -> dict:
+    """One long pair through the strip pipeline (sw_align_long). Returns host ints
+    ``score, ref_end, query_end, flags``; a 16-bit run that hits the wrap guard is
+    repeated in 32 bits."""
+    _require_cuda()
+    L = _lib.load()
+    qd = query_dev if query_dev is not None else torch.from_numpy(
+        _codes(query, scheme.n_symbols, "query")).cuda()
+    rd = ref_dev if ref_dev is not None else torch.from_numpy(
+        _codes(ref, scheme.n_symbols, "reference")).cuda()
+    m, n = int(qd.numel()), int(rd.numel())
+    if m == 0 or n == 0:
+        return {"score": 0, "ref_end": -1, "query_end": -1, "flags": 0}
+    sub = torch.from_numpy(scheme.as_array()).cuda()
+    out = torch.zeros(4, dtype=torch.int32, device="cuda")
+    fl = torch.zeros(1, dtype=torch.uint8, device="cuda")
+    for w in ((16, 32) if width == 16 else (32,)):
+        nbytes = L.sw_long_workspace_bytes(m, n, scheme.n_symbols, w)
+        if nbytes < 0:
+            _lib.check(int(nbytes))
+        ws = torch.empty(int(nbytes), dtype=torch.uint8, device="cuda")
+        _lib.check(L.sw_align_long(w, _kernel_id(kernel), _ptr(qd), m, _ptr(rd), n, _ptr(sub),
+                                   scheme.n_symbols, scheme.gap_open, scheme.gap_extend,
+                                   scheme.bias, scheme.max_score, _ptr(ws), int(nbytes),
+                                   C.c_void_p(out.data_ptr()), C.c_void_p(out.data_ptr() + 4),
+                                   C.c_void_p(out.data_ptr() + 8), _ptr(fl), _stream()))
+        flags = int(fl.item())
+        if not flags & _lib.FLAG_RESCUE:
+            break
+    o = out.cpu().tolist()
+    if width == 16 and w == 32:
+        flags |= _lib.FLAG_RESCUED
+    return {"score": o[0], "ref_end": o[1], "query_end": o[2], "flags": flags & ~_lib.FLAG_RESCUE}
+
+
 def db_align(prof: DeviceProfile, tgt: torch.Tensor, start: torch.Tensor, length: torch.Tensor,
              order: torch.Tensor | None = None, kernel: str = "scan",
-             col_passes: torch.Tensor | None = None, out: dict | None = None) -> dict:
+             col_passes: torch.Tensor | None = None, out: dict | None = None,
+             rescue: bool = True) -> dict:
     """All-device database alignment: one profile vs n targets, 16-bit with a
     device-side 32-bit rescue of wrap-guard hits. Returns dict of device tensors
     ``score, ref_end, query_end, flags`` indexed by target id."""
@@ -220,7 +262,8 @@ def db_align(prof: DeviceProfile, tgt: torch.Tensor, start: torch.Tensor, length
                              _ptr(length), _ptr(order), n, None, _ptr(out["score"]),
                              _ptr(out["ref_end"]), _ptr(out["query_end"]), _ptr(out["flags"]),
                              _ptr(col_passes), st))
-    _rescue_db(prof, tgt, start, length, kid, col_passes, out, n)
+    if rescue:
+        _rescue_db(prof, tgt, start, length, kid, col_passes, out, n)
     return out
 
 
@@ -246,6 +289,11 @@ def _rescue_db(prof, tgt, start, length, kid, col_passes, out, n) -> None:
 def _result_from(prof_or_none, kernel, n, L_, P, score, flags, rend, qend, passes) -> AlignmentResult:
     fl = int(flags)
     passes_np = np.asarray(passes, dtype=np.int64) if passes is not None else np.zeros(n, np.int64)
+    if P == 0:  # strip pipeline: no single reference layout to reconstruct counters for
+        return AlignmentResult(score=int(score), overflow=bool(fl & _lib.FLAG_REF_OVERFLOW),
+                               counters=None, correction_passes=0, column_passes=(),
+                               ref_end=int(rend), query_end=int(qend),
+                               rescued=bool(fl & _lib.FLAG_RESCUED))
     if kernel == "scan":
         passes_np = np.full(n, scan_steps(P), dtype=np.int64)
     cnt = counters_from_passes(kernel, n, L_, P, passes_np) if n > 0 else OpCounters()
@@ -271,12 +319,33 @@ def align_prebuilt(kernel: str, prof: DeviceProfile, bias=None, ref=None,
     r = _codes(ref, prof.scheme.n_symbols, "reference")
     n = int(r.size)
     if n == 0:
-        return _result_from(None, kernel, 0, prof.seg_len, prof.lanes, 0, 0, -1, -1, None)
+        return _result_from(None, kernel, 0, prof.seg_len if prof.plan16 else 0,
+                            prof.lanes if prof.plan16 else 0, 0, 0, -1, -1, None)
+    long_query = prof.plan16 is None
+    if not long_query and prof.plan32 is None:
+        try:
+            prof.ensure32()
+        except _lib.SwError:
+            long_query = None  # 16-bit warp kernel; a rescue would need the strip pipeline
+    if long_query:
+        if kernel != "scan":
+            raise _lib.SwError(_lib.SW_ENOTSUP,
+                               f"query of {prof.m} residues: only the scan kernel runs as a strip pipeline")
+        o = align_long(None, r, prof.scheme, 16, kernel, query_dev=prof.query)
+        return _result_from(None, kernel, n, 0, 0, o["score"], o["flags"], o["ref_end"],
+                            o["query_end"], None)
     tgt = torch.from_numpy(r).cuda()
     start = torch.zeros(1, dtype=torch.int64, device="cuda")
     length = torch.full((1,), n, dtype=torch.int32, device="cuda")
     passes = torch.zeros(n, dtype=torch.int32, device="cuda") if kid != 2 else None
-    out = db_align(prof, tgt, start, length, None, kernel, passes)
+    if long_query is None:
+        out = db_align(prof, tgt, start, length, None, kernel, passes, rescue=False)
+        if int(out["flags"][0]) & _lib.FLAG_RESCUE:
+            o = align_long(None, None, prof.scheme, 32, "scan", query_dev=prof.query, ref_dev=tgt)
+            return _result_from(None, kernel, n, 0, 0, o["score"], o["flags"] | _lib.FLAG_RESCUED,
+                                o["ref_end"], o["query_end"], None)
+    else:
+        out = db_align(prof, tgt, start, length, None, kernel, passes)
     flags = int(out["flags"][0])
     if flags & _lib.FLAG_RESCUED:
         P, L_ = prof.plan32.lanes, prof.plan32.seg_len

@@ -1,5 +1,6 @@
 #define SWB_X_T 16
+#define SWB_X_GE 1
 #define SWB_X_LO 17
 #define SWB_X_HI 32
-#define SWB_X_FILL swb_fill_exact_t16
+#define SWB_X_FILL swb_fill_exact_t16_g1_b
 #include "sw_inst_exact.inc"

@@ -8,7 +8,7 @@
 #include <cstring>
 #include <mutex>
 
-#include "sw_kernels.cuh"
+#include "sw_chain.cuh"
 #include "../../include/swscan_b200.h"
 
 using namespace swb;
@@ -31,15 +31,19 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 KernelTable g_tab[2][3];
 ExactTable g_exact;  // 16-bit scan, exact segment length
+const void* g_chain[2][4];  // strip pipeline [width][L = 4, 8, 16, 32]
+const void* g_chain_prof[2];
 std::once_flag g_once;
 
 void init_tables() {
   std::memset(g_tab, 0, sizeof g_tab);
   std::memset(g_exact, 0, sizeof g_exact);
-  swb_fill_exact_t8a(g_exact);
-  swb_fill_exact_t8b(g_exact);
-  swb_fill_exact_t16(g_exact);
-  swb_fill_exact_t32(g_exact);
+  swb_fill_exact_t8_g0_a(g_exact); swb_fill_exact_t8_g0_b(g_exact);
+  swb_fill_exact_t8_g1_a(g_exact); swb_fill_exact_t8_g1_b(g_exact);
+  swb_fill_exact_t8_g2_a(g_exact); swb_fill_exact_t8_g2_b(g_exact);
+  swb_fill_exact_t16_g0_b(g_exact); swb_fill_exact_t16_g1_b(g_exact); swb_fill_exact_t16_g2_b(g_exact);
+  swb_fill_exact_t32_g0_b(g_exact); swb_fill_exact_t32_g1_b(g_exact); swb_fill_exact_t32_g2_b(g_exact);
+  swb_fill_chain(g_chain, g_chain_prof);
   swb_fill_w16_scan(g_tab[0][VAR_SCAN]);
   swb_fill_w16_lazyf(g_tab[0][VAR_LAZYF]);
   swb_fill_w16_mirror(g_tab[0][VAR_LAZYF_MIRROR]);
@@ -262,7 +266,12 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
   const int li = lmax_index(p->lmax);
   if (li < 0 || kLmaxSet[li] != p->lmax) return fail(SW_EINVAL, "bad plan lmax %d", p->lmax);
   const void* fn = nullptr;
-  if (wi == 0 && var == VAR_SCAN) fn = g_exact[ilog2(p->threads)][p->seg_len];
+  int block = 256;
+  if (wi == 0 && var == VAR_SCAN) {
+    const int gi = (gap_extend == 1 || gap_extend == 2) ? gap_extend : 0;
+    fn = g_exact[gi][ilog2(p->threads)][p->seg_len];
+    if (fn) block = 128;
+  }
   if (!fn) fn = g_tab[wi][var][ilog2(p->threads)][li];
   if (!fn) return fail(SW_ENOTSUP, "no kernel for width %d, threads %d", p->width, p->threads);
   SwArgs a;
@@ -291,7 +300,7 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
   const size_t smem = (size_t)p->prof_words * 4;
   const int G = 32 / p->threads;
   const int64_t tasks = d_n_jobs ? 0 : (n + G - 1) / G;
-  return launch(fn, a, smem, 256, tasks, (cudaStream_t)stream);
+  return launch(fn, a, smem, block, tasks, (cudaStream_t)stream);
 }
 
 int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8_t* d_qry,
@@ -324,7 +333,12 @@ int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8
   const void* fn = nullptr;
   // every query of the batch has the same segment length: exact-L instance
   const bool uniform_L = min_qlen > 0 && (min_qlen + p.lanes - 1) / p.lanes == p.seg_len;
-  if (wi == 0 && var == VAR_SCAN && uniform_L) fn = g_exact[ilog2(p.threads)][p.seg_len];
+  int max_block = 256;
+  if (wi == 0 && var == VAR_SCAN && uniform_L && !per_pair) {
+    const int gi = (gap_extend == 1 || gap_extend == 2) ? gap_extend : 0;
+    fn = g_exact[gi][ilog2(p.threads)][p.seg_len];
+    if (fn) max_block = 128;
+  }
   if (!fn) fn = g_tab[wi][var][ilog2(p.threads)][lmax_index(p.lmax)];
   if (!fn) return fail(SW_ENOTSUP, "no kernel for width %d, threads %d", width, p.threads);
   SwArgs a;
@@ -357,7 +371,7 @@ int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8
   a.col_passes = d_col_passes;
   a.pair_stride = (n_sym + 1) * p.seg_len * p.threads;
   // block size: as many warps as the per-group profile slices allow (<= 256 threads)
-  int block = 256;
+  int block = max_block;
   const size_t per_thread = (size_t)(n_sym + 1) * p.seg_len * 4;  // slice bytes / T
   while (block > 32 && per_thread * block > 110 * 1024) block >>= 1;
   const size_t smem = per_thread * block;
@@ -365,6 +379,123 @@ int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8
   const int G = 32 / p.threads;
   const int64_t tasks = d_n_jobs ? 0 : (n + G - 1) / G;
   return launch(fn, a, smem, block, tasks, (cudaStream_t)stream);
+}
+
+// strip-pipeline geometry: per-column latency model t(L) ~ 190 + 5 L cycles,
+// total ~ (n + nb*K) * t(L); prefer the smallest total.
+struct ChainGeo {
+  int li, L, nb;
+  size_t prof_words, ring_bytes, total;
+};
+
+static ChainGeo chain_geo(int64_t m, int64_t n, int n_sym, int width) {
+  const int lpw = width == 16 ? 2 : 1;
+  static const int Ls[4] = {4, 8, 16, 32};
+  ChainGeo g{};
+  double best = 1e300;
+  for (int li = 0; li < 4; ++li) {
+    const int L = Ls[li];
+    const int64_t rows = 32LL * lpw * L;
+    const int64_t nb = (m + rows - 1) / rows;
+    const double cost = (double)(n + nb * kChainK) * (190.0 + 5.0 * L);
+    if (cost < best) {
+      best = cost;
+      g.li = li; g.L = L; g.nb = (int)(nb < 1 ? 1 : nb);
+    }
+  }
+  g.prof_words = (size_t)g.nb * (n_sym + 1) * g.L * 32;
+  g.ring_bytes = (size_t)g.nb * kChainRing * kChainK * sizeof(int2);
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  g.total = al(g.prof_words * 4) + al(g.ring_bytes) + al(g.nb * 8) * 2 + al(g.nb * 16) + 256;
+  return g;
+}
+
+int64_t sw_long_workspace_bytes(int64_t m, int64_t n, int32_t n_sym, int32_t width) {
+  if ((width != 16 && width != 32) || n_sym < 1 || n_sym > kMaxSym || m < 1)
+    return fail(SW_EINVAL, "bad long-pair shape");
+  return (int64_t)chain_geo(m, n, n_sym, width).total;
+}
+
+int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int64_t m,
+                      const uint8_t* d_ref, int64_t n, const int8_t* d_sub, int32_t n_sym,
+                      int32_t gap_open, int32_t gap_extend, int32_t bias, int32_t max_sub,
+                      void* d_workspace, int64_t workspace_bytes, int32_t* d_score,
+                      int32_t* d_ref_end, int32_t* d_query_end, uint8_t* d_flags,
+                      sw_stream_t stream) {
+  std::call_once(g_once, init_tables);
+  if (!d_query || !d_ref || !d_sub || !d_workspace || !d_score) return fail(SW_EINVAL, "NULL argument");
+  if (width != 16 && width != 32) return fail(SW_EINVAL, "width must be 16 or 32");
+  if (kernel != SW_KERNEL_SCAN) return fail(SW_ENOTSUP, "the strip pipeline runs the scan kernel only");
+  if (!(gap_open >= gap_extend && gap_extend >= 1)) return fail(SW_EINVAL, "require gap_open >= gap_extend >= 1");
+  if (m < 1 || n < 1) return fail(SW_EINVAL, "empty sequence");
+  if (n_sym < 1 || n_sym > kMaxSym) return fail(SW_ENOTSUP, "alphabet size %d", n_sym);
+  const ChainGeo g = chain_geo(m, n, n_sym, width);
+  if ((size_t)workspace_bytes < g.total) return fail(SW_EINVAL, "workspace too small (%zu B needed)", g.total);
+  const int wi = width == 16 ? 0 : 1;
+  cudaStream_t s = (cudaStream_t)stream;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  char* ws = (char*)d_workspace;
+  uint32_t* prof = (uint32_t*)ws;
+  ws += al(g.prof_words * 4);
+  int2* ring = (int2*)ws;
+  ws += al(g.ring_bytes);
+  char* zero_begin = ws;
+  unsigned long long* published = (unsigned long long*)ws;
+  ws += al(g.nb * 8);
+  unsigned long long* consumed = (unsigned long long*)ws;
+  ws += al(g.nb * 8);
+  int4* best = (int4*)ws;
+  ws += al(g.nb * 16);
+  unsigned int* done = (unsigned int*)ws;
+  ws += 256;
+  cudaError_t e = cudaMemsetAsync(zero_begin, 0, (size_t)(ws - zero_begin), s);
+  if (e != cudaSuccess) return cuda_fail(e, "memset chain workspace");
+  {
+    int A = n_sym, L = g.L, nb = g.nb, mm = (int)m;
+    void* pargs[] = {(void*)&d_query, (void*)&mm, (void*)&d_sub, (void*)&A, (void*)&L,
+                     (void*)&nb, (void*)&bias, (void*)&prof};
+    const int words = (int)g.prof_words;
+    e = cudaLaunchKernel(g_chain_prof[wi], dim3((words + 255) / 256), dim3(256), pargs, 0, s);
+    if (e != cudaSuccess) return cuda_fail(e, "sw_chain_profile_kernel");
+  }
+  ChainArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.prof = prof;
+  a.n_sym = n_sym;
+  a.m = (int)m;
+  a.nb = g.nb;
+  a.ref = d_ref;
+  a.n = n;
+  a.go = gap_open;
+  a.ge = gap_extend;
+  a.bias = bias;
+  a.max_sub = max_sub;
+  a.ring = ring;
+  a.published = published;
+  a.consumed = consumed;
+  a.best = best;
+  a.done = done;
+  a.score = d_score;
+  a.ref_end = d_ref_end;
+  a.query_end = d_query_end;
+  a.flags = d_flags;
+  const void* fn = g_chain[wi][g.li];
+  const size_t smem = (size_t)(n_sym + 1) * g.L * 32 * 4;
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(chain smem)");
+  }
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "chain occupancy");
+  if ((int64_t)occ * sms < g.nb)
+    return fail(SW_ENOTSUP, "%d query strips cannot be co-resident (%d per SM x %d SMs)", g.nb, occ, sms);
+  void* params[] = {(void*)&a};
+  e = cudaLaunchCooperativeKernel(fn, dim3(g.nb), dim3(32), params, smem, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchCooperativeKernel(sw_chain_kernel)");
+  return SW_OK;
 }
 
 int32_t sw_collect_flagged(const uint8_t* d_flags, int64_t n, uint8_t mask, int32_t* d_list,

@@ -1,0 +1,287 @@
+// sw_chain.cuh -- long single pairs: a pipeline of query strips.
+//
+// The query is cut into NB strips of M = P*L positions; strip b is owned by
+// one warp-sized CTA (P = 32 lanes in 32-bit, 64 in 16-bit), which streams
+// every reference residue (column) through the same striped recurrence and
+// Alg. 6 scan as the single-warp kernels (sw_kernels.cuh).  The only coupling
+// between strips is one boundary value pair per column, produced by strip b-1
+// and consumed by strip b:
+//   F_out[i]  -- the true vertical-gap value leaving strip b-1 in column i,
+//                folded into strip b's carry: carry[l] = max(carry_local[l],
+//                F_in - l*L*ge)  (one DPX op);
+//   H_last[i] -- the corrected H of strip b-1's last cell in column i, the
+//                diagonal input of strip b's first cell in column i+1.
+// Boundary values move in tiles of K columns through a ring buffer in global
+// memory (L2) with release/acquire progress counters and back-pressure; all
+// strips are co-resident (cooperative launch), strip b runs one tile behind
+// strip b-1.  The per-strip best (score, first column, first query position)
+// is reduced by the last strip to finish.
+#pragma once
+#include "sw_kernels.cuh"
+
+namespace swb {
+
+constexpr int kChainK = 32;     // columns per handoff tile
+constexpr int kChainRing = 8;   // tiles in flight per boundary
+
+struct ChainArgs {
+  const uint32_t* prof;   // [(A+1)][L][32] words, striped per strip (see sw_chain_profile_kernel)
+  int32_t n_sym;
+  int32_t m;              // query length
+  int32_t nb;             // strips
+  const uint8_t* ref;
+  int64_t n;              // reference length
+  int32_t go, ge, bias, max_sub;
+  int32_t early_exit;
+  // workspace (zeroed before launch)
+  int2* ring;                     // [nb][kChainRing*kChainK] (F_out, H_last)
+  unsigned long long* published;  // [nb] columns published by strip b
+  unsigned long long* consumed;   // [nb] columns consumed by strip b (from strip b-1)
+  int4* best;                     // [nb] per-strip (score, col, q, 0)
+  unsigned int* done;             // [1] ticket
+  // outputs
+  int32_t* score;
+  int32_t* ref_end;
+  int32_t* query_end;
+  uint8_t* flags;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void wait_ge(const unsigned long long* p, unsigned long long want) {
+  if (ld_acquire(p) >= want) return;
+  unsigned ns = 32;
+  while (ld_acquire(p) < want) {
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+  }
+}
+
+// Chain profile: strip-major layout prof[b][(A+1)][L][32] so each CTA reads one contiguous slab.
+template <class Wd>
+__global__ void sw_chain_profile_kernel(const uint8_t* __restrict__ query, int m,
+                                        const int8_t* __restrict__ sub, int A, int L, int nb,
+                                        int bias, uint32_t* __restrict__ prof) {
+  constexpr int P = 32 * Wd::LPW;
+  const int words = nb * (A + 1) * L * 32;
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
+    const int t = w & 31;
+    const int j = (w >> 5) % L;
+    const int sym = (w / (32 * L)) % (A + 1);
+    const int b = w / (32 * L * (A + 1));
+    int v[2] = {0, 0};
+#pragma unroll
+    for (int h = 0; h < Wd::LPW; ++h) {
+      const int q = b * P * L + (h * 32 + t) * L + j;
+      if (sym == A) v[h] = Wd::NULLV;
+      else if (q >= m) v[h] = -bias;
+      else v[h] = sub[sym * A + query[q]];
+    }
+    prof[w] = Wd::pack(v[0], v[1]);
+  }
+}
+
+template <class Wd, int L, int VAR>
+__global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
+  static_assert(VAR == VAR_SCAN, "the strip pipeline implements the scan kernel");
+  constexpr int T = 32;
+  constexpr int P = T * Wd::LPW;
+  constexpr int STEPS = ceil_log2(P);
+  constexpr int RING = kChainRing * kChainK;
+  const int t = threadIdx.x;
+  const int b = blockIdx.x;
+  const int nb = a.nb;
+  const uint32_t gmask = 0xffffffffu;
+  const int A = a.n_sym;
+
+  // profile slab of this strip -> shared memory
+  extern __shared__ uint32_t smem[];
+  {
+    const int words = (A + 1) * L * 32;
+    const uint32_t* src = a.prof + (size_t)b * words;
+    for (int w = t; w < words; w += 32) smem[w] = __ldg(src + w);
+    __syncwarp();
+  }
+  const uint32_t* prof_t = smem + t;
+
+  uint32_t sel[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) sel[s] = Wd::shift_sel(t, 1 << s);
+  const int cl = Wd::CLAMP;
+  const int go = a.go, ge = a.ge;
+  const uint32_t NGO = Wd::splat(-min(go, cl));
+  const uint32_t NGE = Wd::splat(-min(ge, cl));
+  const uint32_t NWRAP = Wd::splat(-(int)min((int64_t)(L - 1) * ge, (int64_t)cl));
+  const uint32_t NLD = Wd::splat(-(int)min((int64_t)L * ge, (int64_t)cl));
+  uint32_t NJ[L];
+#pragma unroll
+  for (int c = 0; c < L; ++c) NJ[c] = Wd::splat(-(int)min((int64_t)c * ge, (int64_t)cl));
+  uint32_t NKD[STEPS];
+#pragma unroll
+  for (int s = 0; s < STEPS; ++s)
+    NKD[s] = Wd::splat(-(int)min((int64_t)(1 << s) * L * (int64_t)ge, (int64_t)cl));
+  // decay of the incoming strip F to this thread's lanes: lane * L * ge
+  const uint32_t NLANE = Wd::pack(-(int)min((int64_t)t * L * ge, (int64_t)cl),
+                                  -(int)min((int64_t)(T + t) * L * ge, (int64_t)cl));
+
+  uint32_t H[L], E[L];
+#pragma unroll
+  for (int c = 0; c < L; ++c) { H[c] = 0u; E[c] = 0u; }
+  uint32_t carry = 0u, wnext = 0u;
+  uint32_t tb = 0u;
+  int bcol[2] = {-1, -1}, bq[2] = {-1, -1};
+  const int64_t n = a.n;
+  const int64_t qbase = (int64_t)b * P * L;
+  int hd_prev = 0;  // H_last of strip b-1 for the previous column
+
+  int2* ring_in = a.ring + (size_t)(b > 0 ? b - 1 : 0) * RING;
+  int2* ring_out = a.ring + (size_t)b * RING;
+
+  for (int64_t t0 = 0; t0 < n; t0 += kChainK) {
+    const int kc = (int)min((int64_t)kChainK, n - t0);
+    // ---- incoming boundary tile ----
+    int fin_l = 0, hl_l = 0;
+    if (b > 0) {
+      if (t == 0) wait_ge(a.published + (b - 1), (unsigned long long)(t0 + kc));
+      __syncwarp();
+      if (t < kc) {
+        const int2 v = __ldcg(ring_in + ((t0 + t) % RING));
+        fin_l = v.x;
+        hl_l = v.y;
+      }
+      __syncwarp();
+      if (t == 0) st_release(a.consumed + b, (unsigned long long)(t0 + kc));
+    }
+    // ---- back-pressure before producing this tile ----
+    if (b + 1 < nb && t == 0 && t0 >= RING)
+      wait_ge(a.consumed + (b + 1), (unsigned long long)(t0 - RING + kc));
+    __syncwarp();
+    int fo_l = 0, ho_l = 0;  // this tile's outgoing values (lane k holds column t0+k)
+
+    for (int k = 0; k < kc; ++k) {
+      const int64_t i = t0 + k;
+      const int sym = (int)__ldg(a.ref + i);
+      const uint32_t* pr = prof_t + sym * (L * 32);
+      const int fin = __shfl_sync(gmask, fin_l, k);
+      const int hlk = __shfl_sync(gmask, hl_l, k);
+      // diagonal for the strip's first cell: corrected H of strip b-1, column i-1
+      uint32_t vh = Wd::template shift<T, 1>(wnext, t, gmask, sel[0]);
+      if (t == 0) {  // lane 0 (low half of thread 0) takes the previous strip's value
+        constexpr uint32_t keep = Wd::LPW == 2 ? 0xffff0000u : 0u;
+        vh = (vh & keep) | (Wd::pack(hd_prev, 0) & ~keep);
+      }
+      hd_prev = hlk;
+      uint32_t F = 0u, cm = 0u;
+#pragma unroll
+      for (int c = 0; c < L; ++c) {
+        const uint32_t S = pr[c * 32];
+        const uint32_t u = Wd::addmax(vh, S, E[c]);
+        const uint32_t Hn = Wd::vmax(u, F);
+        const uint32_t Xu = Wd::add(u, NGO);
+        E[c] = Wd::addmax_relu(E[c], NGE, Xu);
+        F = Wd::addmax_relu(F, NGE, Xu);
+        cm = Wd::vmax(cm, u);
+        vh = Wd::addmax(carry, NJ[c], H[c]);
+        H[c] = Hn;
+      }
+      // end coordinates (first strict improvement per lane)
+      const uint32_t nbst = Wd::vmax(tb, cm);
+      if (nbst != tb) {
+#pragma unroll
+        for (int h = 0; h < Wd::LPW; ++h) {
+          const int cv = Wd::get(cm, h);
+          if (cv > Wd::get(tb, h)) {
+            int jj = L - 1;
+#pragma unroll
+            for (int c = L - 1; c >= 0; --c)
+              if (Wd::get(H[c], h) >= cv) jj = c;
+            bcol[h] = (int)i;
+            bq[h] = (int)(qbase + (h * T + t) * L + jj);
+          }
+        }
+        tb = nbst;
+      }
+      // Alg. 6 scan inside the strip, then fold in the strip's incoming F
+      uint32_t acc = Wd::template shift<T, 1>(F, t, gmask, sel[0]);
+#pragma unroll
+      for (int s = 0; s < STEPS; ++s) {
+        // K = 1 << s, dispatched statically
+        if (s == 0) acc = Wd::addmax_relu(Wd::template shift<T, 1>(acc, t, gmask, sel[0]), NKD[0], acc);
+        if (s == 1) acc = Wd::addmax_relu(Wd::template shift<T, 2>(acc, t, gmask, sel[1]), NKD[1], acc);
+        if (s == 2) acc = Wd::addmax_relu(Wd::template shift<T, 4>(acc, t, gmask, sel[2]), NKD[2], acc);
+        if (s == 3) acc = Wd::addmax_relu(Wd::template shift<T, 8>(acc, t, gmask, sel[3]), NKD[3], acc);
+        if (s == 4) acc = Wd::addmax_relu(Wd::template shift<T, 16>(acc, t, gmask, sel[4]), NKD[4], acc);
+        if constexpr (Wd::LPW == 2)
+          if (s == 5) acc = Wd::addmax_relu(Wd::template shift<T, 32>(acc, t, gmask, sel[5]), NKD[5], acc);
+      }
+      carry = Wd::addmax(Wd::splat(fin), NLANE, acc);
+      wnext = Wd::addmax(carry, NWRAP, H[L - 1]);       // corrected H of the last word
+      const uint32_t fo = Wd::addmax(carry, NLD, F);    // true F leaving each lane
+      if (t == T - 1) {
+        fo_l = Wd::get(fo, Wd::LPW - 1);
+        ho_l = Wd::get(wnext, Wd::LPW - 1);
+        if (b + 1 < nb) ring_out[i % RING] = make_int2(fo_l, ho_l);
+      }
+    }
+    if (b + 1 < nb) {
+      __syncwarp();
+      if (t == T - 1) {
+        __threadfence();
+        st_release(a.published + b, (unsigned long long)(t0 + kc));
+      }
+    }
+    (void)fo_l;
+    (void)ho_l;
+  }
+
+  // ---- per-strip best, then the last strip to finish reduces ----
+  int best = Wd::get(tb, 0), col = bcol[0], q = bq[0];
+  if constexpr (Wd::LPW == 2) {
+    const int b1 = Wd::get(tb, 1);
+    if (b1 > best || (b1 == best && (bcol[1] < col || (bcol[1] == col && bq[1] < q)))) {
+      best = b1; col = bcol[1]; q = bq[1];
+    }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const int ob = __shfl_xor_sync(gmask, best, off);
+    const int oc = __shfl_xor_sync(gmask, col, off);
+    const int oq = __shfl_xor_sync(gmask, q, off);
+    if (ob > best || (ob == best && (oc < col || (oc == col && oq < q)))) {
+      best = ob; col = oc; q = oq;
+    }
+  }
+  if (t == 0) {
+    a.best[b] = make_int4(best, col, q, 0);
+    __threadfence();
+    const unsigned ticket = atomicAdd(a.done, 1u);
+    if (ticket == (unsigned)nb - 1) {
+      __threadfence();
+      for (int s = 0; s < nb; ++s) {
+        const int4 r = __ldcg(a.best + s);
+        if (r.x > best || (r.x == best && (r.y < col || (r.y == col && r.z < q)))) {
+          best = r.x; col = r.y; q = r.z;
+        }
+      }
+      uint8_t fl = 0;
+      if constexpr (Wd::LPW == 2) {
+        if (best >= 32767 - a.max_sub) fl |= FLAG_RESCUE;
+      }
+      if (best > 65535 - a.bias) fl |= FLAG_REF_OVERFLOW;
+      if (best == 0) { col = -1; q = -1; }
+      a.score[0] = best;
+      if (a.ref_end) a.ref_end[0] = col;
+      if (a.query_end) a.query_end[0] = q;
+      if (a.flags) a.flags[0] = fl;
+    }
+  }
+}
+
+}  // namespace swb

@@ -180,9 +180,11 @@ struct SwArgs {
   X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29)  \
   X(30) X(31)
 
-template <class Wd, int T, int LMAX, int VAR, bool EXACT = false>
-__global__ void __launch_bounds__(256)
+template <class Wd, int T, int LMAX, int VAR, bool EXACT = false, int GE = 0>
+__global__ void __launch_bounds__(EXACT ? 128 : 256, EXACT ? 4 : 1)
 sw_striped_kernel(const SwArgs a) {
+  // GE > 0: gap-extend penalty known at compile time, so every decay constant
+  // (j*ge, k*L*ge) is an immediate operand of VIADDMNMX instead of a register.
   // EXACT: LMAX is the segment length itself (uniform-L launches); the word
   // loop is straight-line code the scheduler can software-pipeline.
   static_assert(LMAX >= 1 && LMAX <= 32, "LMAX");
@@ -218,7 +220,8 @@ sw_striped_kernel(const SwArgs a) {
   uint32_t NKD[STEPS];
   int bias = a.bias, max_sub = a.max_sub;
 
-  auto set_gaps = [&](int go, int ge, int L_) {
+  auto set_gaps = [&](int go, int ge_rt, int L_) {
+    const int ge = GE > 0 ? GE : ge_rt;
     const int cl = Wd::CLAMP;
     NGO = Wd::splat(-min(go, cl));
     NGE = Wd::splat(-min(ge, cl));
@@ -317,9 +320,14 @@ sw_striped_kernel(const SwArgs a) {
       nxt = (i + 1 < len) ? (int)__ldg(tp + i + 1) : nullsym;
       const uint32_t* pr = prof_base + sym * LT;
 
+      // scan path: the whole warp is converged here, so shuffles take the full
+      // mask (width T keeps the data inside the group) and skip the runtime
+      // convergence checks a sub-warp mask costs; lazy-F passes diverge per group.
+      constexpr bool kConverged = VAR == VAR_SCAN;
+      const uint32_t cmask = kConverged ? 0xffffffffu : gmask;
       uint32_t w = H[LMAX - 1];
       if constexpr (VAR == VAR_SCAN) w = Wd::addmax(carry, NWRAP, w);
-      uint32_t vh = Wd::template shift<T, 1>(w, t, gmask, sel[0]);
+      uint32_t vh = Wd::template shift<T, 1>(w, t, cmask, sel[0]);
       uint32_t F = 0u, cm = 0u;
 
 #define SWB_WORD_BODY(C)                                                   \
@@ -375,11 +383,11 @@ sw_striped_kernel(const SwArgs a) {
 
       // ---- cross-lane F dependency ----
       if constexpr (VAR == VAR_SCAN) {
-        uint32_t acc = Wd::template shift<T, 1>(F, t, gmask, sel[0]);
+        uint32_t acc = Wd::template shift<T, 1>(F, t, cmask, sel[0]);
         // Alg. 6 weighted max-scan, k = 1, 2, 4, ... (src/_compiled.py:320-336)
 #define SWB_STEP(S)                                                                         \
   if constexpr ((S) < STEPS) {                                                             \
-    acc = Wd::addmax_relu(Wd::template shift<T, (1 << (S))>(acc, t, gmask, sel[S]), NKD[S], \
+    acc = Wd::addmax_relu(Wd::template shift<T, (1 << (S))>(acc, t, cmask, sel[S]), NKD[S], \
                           acc);                                                            \
   }
         SWB_STEP(0) SWB_STEP(1) SWB_STEP(2) SWB_STEP(3) SWB_STEP(4) SWB_STEP(5)
@@ -542,11 +550,14 @@ void swb_fill_w32_scan(swb::KernelTable& t);
 void swb_fill_w32_lazyf(swb::KernelTable& t);
 void swb_fill_w32_mirror(swb::KernelTable& t);
 
-// exact-L instances (uniform segment length): [log2 T][L]
+// exact-L instances (uniform segment length): [ge specialisation 0=runtime,1,2][log2 T][L]
 namespace swb {
-using ExactTable = const void* [kNumT][33];
+constexpr int kNumGe = 3;
+using ExactTable = const void* [kNumGe][kNumT][33];
 }
-void swb_fill_exact_t8a(swb::ExactTable& t);
-void swb_fill_exact_t8b(swb::ExactTable& t);
-void swb_fill_exact_t16(swb::ExactTable& t);
-void swb_fill_exact_t32(swb::ExactTable& t);
+#define SWB_X_DECL(T, GE, PART) void swb_fill_exact_t##T##_g##GE##_##PART(swb::ExactTable& t);
+SWB_X_DECL(8, 0, a) SWB_X_DECL(8, 0, b) SWB_X_DECL(8, 1, a) SWB_X_DECL(8, 1, b)
+SWB_X_DECL(8, 2, a) SWB_X_DECL(8, 2, b) SWB_X_DECL(16, 0, b) SWB_X_DECL(16, 1, b)
+SWB_X_DECL(16, 2, b) SWB_X_DECL(32, 0, b) SWB_X_DECL(32, 1, b) SWB_X_DECL(32, 2, b)
+#undef SWB_X_DECL
+void swb_fill_chain(const void* (&tab)[2][4], const void* (&ptab)[2]);

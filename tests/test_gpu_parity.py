@@ -254,3 +254,52 @@ def test_random_schemes_and_layouts(A, oracle):
                 assert (r["score"] == s).all(), (trial, kern, width)
                 assert (r["ref_end"] == re_).all(), (trial, kern, width)
                 assert (r["query_end"] == qe).all(), (trial, kern, width)
+
+
+# ---- long pairs: the strip pipeline -------------------------------------------------
+
+
+def test_long_pair_pipeline_int32_config4(A, oracle):
+    from paper_1909_00899_b200 import workloads as W
+
+    w = W.config4()
+    want = oracle.scalar(w.query, w.ref, w.scheme.as_array(), 2, 1)
+    for width in (32, 16):
+        r = A.align_long(w.query, w.ref, w.scheme, width=width)
+        assert (r["score"], r["ref_end"], r["query_end"]) == want, width
+
+
+def test_long_pair_pipeline_config5_slice(A, oracle):
+    from paper_1909_00899_b200 import workloads as W
+
+    g = golden("configs.npz")
+    w = W.config5(m=8192, n=131_072, block=7_500)
+    want = oracle.scalar(w.query, w.ref, w.scheme.as_array(), 3, 1)
+    assert want[0] == int(g["c5slice_scalar"])
+    r = A.align_long(w.query, w.ref, w.scheme, width=32)
+    assert (r["score"], r["ref_end"], r["query_end"]) == want
+    r = A.align_pair("scan", 0, w.query, w.ref, w.scheme)
+    assert (r.score, r.ref_end, r.query_end) == want
+
+
+def test_long_pair_pipeline_random(A, oracle):
+    from paper_1909_00899_b200.scoring import ScoringScheme
+
+    rng = np.random.default_rng(0x10C)
+    for trial in range(10):
+        k = int(rng.integers(2, 21))
+        mat = rng.integers(-5, 6, (k, k))
+        go = int(rng.integers(1, 12))
+        ge = int(rng.integers(1, go + 1))
+        sch = ScoringScheme.from_array(mat, go, ge)
+        m = int(rng.integers(1, 9000))
+        n = int(rng.integers(1, 3000))
+        q = rng.integers(0, k, m).astype(np.uint8)
+        r = rng.integers(0, k, n).astype(np.uint8)
+        if trial % 2:  # plant a homologous block so the best alignment is long
+            blk = q[: min(m, n)]
+            r[: blk.shape[0]] = blk
+        want = oracle.scalar(q, r, mat, go, ge)
+        for width in (16, 32):
+            got = A.align_long(q, r, sch, width=width)
+            assert (got["score"], got["ref_end"], got["query_end"]) == want, (trial, width, m, n)
