@@ -135,8 +135,8 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
 #pragma unroll
   for (int c = 0; c < L; ++c) { H[c] = 0u; E[c] = 0u; }
   uint32_t carry = 0u, wnext = 0u;
-  uint32_t tb = 0u;
-  int bcol[2] = {-1, -1}, bq[2] = {-1, -1};
+  int gb = 0;                      // best of all earlier columns in this strip
+  int bv = 0, bcol = -1, bq = -1;  // this thread's first-maximum record
   const int64_t n = a.n;
   const int64_t qbase = (int64_t)b * P * L;
   int hd_prev = 0;  // H_last of strip b-1 for the previous column
@@ -191,22 +191,33 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
         vh = Wd::addmax(carry, NJ[c], H[c]);
         H[c] = Hn;
       }
-      // end coordinates (first strict improvement per lane)
-      const uint32_t nbst = Wd::vmax(tb, cm);
-      if (nbst != tb) {
+      // end coordinates: as sw_striped_kernel, gated on the strip's running best
+      // (a strip-local bound is weaker than the global one, so no event is lost)
+      const int cmx = Wd::hmax(cm);
+      if (cmx > gb) {
+        int jw[2] = {L, L};
+#pragma unroll
+        for (int c = L - 1; c >= 0; --c) {
+          bool p0, p1;
+          Wd::ge2(H[c], cm, p0, p1);
+          if (p0) jw[0] = c;
+          if (p1) jw[1] = c;
+        }
 #pragma unroll
         for (int h = 0; h < Wd::LPW; ++h) {
           const int cv = Wd::get(cm, h);
-          if (cv > Wd::get(tb, h)) {
-            int jj = L - 1;
-#pragma unroll
-            for (int c = L - 1; c >= 0; --c)
-              if (Wd::get(H[c], h) >= cv) jj = c;
-            bcol[h] = (int)i;
-            bq[h] = (int)(qbase + (h * T + t) * L + jj);
+          if (cv > gb && cv > bv) {
+            bv = cv;
+            bcol = (int)i;
+            bq = (int)(qbase + (h * T + t) * L + (jw[h] < L ? jw[h] : 0));
           }
         }
-        tb = nbst;
+      }
+      {
+        int g = max(gb, cmx);
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) g = max(g, __shfl_xor_sync(gmask, g, off));
+        gb = g;
       }
       // Alg. 6 scan inside the strip, then fold in the strip's incoming F
       uint32_t acc = Wd::template shift<T, 1>(F, t, gmask, sel[0]);
@@ -242,13 +253,7 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
   }
 
   // ---- per-strip best, then the last strip to finish reduces ----
-  int best = Wd::get(tb, 0), col = bcol[0], q = bq[0];
-  if constexpr (Wd::LPW == 2) {
-    const int b1 = Wd::get(tb, 1);
-    if (b1 > best || (b1 == best && (bcol[1] < col || (bcol[1] == col && bq[1] < q)))) {
-      best = b1; col = bcol[1]; q = bq[1];
-    }
-  }
+  int best = bv, col = bcol, q = bq;
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
     const int ob = __shfl_xor_sync(gmask, best, off);

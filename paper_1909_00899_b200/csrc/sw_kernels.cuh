@@ -80,6 +80,11 @@ struct W16 {
   __device__ static __forceinline__ uint32_t pack(int lo, int hi) {
     return (uint32_t)(lo & 0xffff) | ((uint32_t)hi << 16);
   }
+  __device__ static __forceinline__ int hmax(uint32_t v) { return max(get(v, 0), get(v, 1)); }
+  // per-lane (v >= k) as two predicates, one DPX instruction (VIMNMX.S16x2 with predicate out)
+  __device__ static __forceinline__ void ge2(uint32_t v, uint32_t k, bool& p0, bool& p1) {
+    (void)__vibmax_s16x2(v, k, &p1, &p0);
+  }
   // shift up by K virtual lanes inside a group of T threads: out[l] = v[l-K], 0 for l < K.
   // `sel` is this thread's PRMT selector for K (identity when t >= K).
   template <int T, int K>
@@ -115,6 +120,11 @@ struct W32 {
   }
   __device__ static __forceinline__ int get(uint32_t v, int) { return (int)v; }
   __device__ static __forceinline__ uint32_t pack(int lo, int) { return (uint32_t)lo; }
+  __device__ static __forceinline__ int hmax(uint32_t v) { return (int)v; }
+  __device__ static __forceinline__ void ge2(uint32_t v, uint32_t k, bool& p0, bool& p1) {
+    p0 = (int)v >= (int)k;
+    p1 = false;
+  }
   template <int T, int K>
   __device__ static __forceinline__ uint32_t shift(uint32_t v, int t, uint32_t gmask, uint32_t) {
     static_assert(K < T, "32-bit lanes shift inside the group");
@@ -310,8 +320,8 @@ sw_striped_kernel(const SwArgs a) {
 #pragma unroll
     for (int c = 0; c < LMAX; ++c) { H[c] = 0u; E[c] = 0u; }
     uint32_t carry = 0u;
-    uint32_t tb = 0u;  // per-lane best (packed)
-    int bcol[2] = {-1, -1}, bq[2] = {-1, -1};
+    int gb = 0;                       // best of all earlier columns, group-wide
+    int bv = 0, bcol = -1, bq = -1;   // this thread's first-maximum record
     const int nullsym = A;
     int nxt = (len > 0) ? (int)__ldg(tp) : nullsym;
 
@@ -363,22 +373,40 @@ sw_striped_kernel(const SwArgs a) {
 #undef SWB_WORD
 #undef SWB_WORD_BODY
 
-      // ---- end-coordinate bookkeeping (first strict improvement per lane) ----
-      const uint32_t nb = Wd::vmax(tb, cm);
-      if (nb != tb) {
+      // ---- end coordinates --------------------------------------------------
+      // The first cell (reference-major order) reaching the final best must
+      // exceed every value of the earlier columns, so only columns whose max
+      // beats the group's running best `gb` need the position search (rare:
+      // the alignment's best grows a few dozen times, not per lane-column).
+      // A cell attaining the best is a diagonal cell, so its stored H equals
+      // u; the first word with H >= cm is the first such cell in the lane.
+      const int cmx = Wd::hmax(cm);
+      if (cmx > gb) {
+        int jw[2] = {LMAX, LMAX};
+#pragma unroll
+        for (int c = LMAX - 1; c >= 0; --c) {
+          if (c >= first) {
+            bool p0, p1;
+            Wd::ge2(H[c], cm, p0, p1);
+            if (p0) jw[0] = c;
+            if (p1) jw[1] = c;
+          }
+        }
 #pragma unroll
         for (int h = 0; h < Wd::LPW; ++h) {
           const int cv = Wd::get(cm, h);
-          if (cv > Wd::get(tb, h)) {
-            int jj = LMAX - 1;
-#pragma unroll
-            for (int c = LMAX - 1; c >= 0; --c)
-              if (c >= first && Wd::get(H[c], h) >= cv) jj = c;
-            bcol[h] = i;
-            bq[h] = (h * T + t) * L + (jj - first);
+          if (cv > gb && cv > bv) {
+            bv = cv;
+            bcol = i;
+            bq = (h * T + t) * L + ((jw[h] < LMAX ? jw[h] : first) - first);
           }
         }
-        tb = nb;
+      }
+      {
+        int g = max(gb, cmx);
+#pragma unroll
+        for (int off = T / 2; off >= 1; off >>= 1) g = max(g, __shfl_xor_sync(cmask, g, off, T));
+        gb = g;
       }
 
       // ---- cross-lane F dependency ----
@@ -430,13 +458,7 @@ sw_striped_kernel(const SwArgs a) {
     }
 
     // ---- reduce (best desc, ref_end asc, query_end asc) over the group ----
-    int best = Wd::get(tb, 0), col = bcol[0], q = bq[0];
-    if constexpr (Wd::LPW == 2) {
-      const int b1 = Wd::get(tb, 1);
-      if (b1 > best || (b1 == best && (bcol[1] < col || (bcol[1] == col && bq[1] < q)))) {
-        best = b1; col = bcol[1]; q = bq[1];
-      }
-    }
+    int best = bv, col = bcol, q = bq;
 #pragma unroll
     for (int off = T / 2; off >= 1; off >>= 1) {
       const int ob = __shfl_xor_sync(gmask, best, off, T);

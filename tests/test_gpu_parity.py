@@ -212,8 +212,8 @@ def test_overflow_rescued_exactly(A):
     for kern in ("scan", "lazyf"):
         r = A.align_pair(kern, 0, q[:1500], q, sch)
         assert r.score == 15_000 and not r.rescued
-        r = A.align_pair(kern, 0, q[:2000], q[:20_000], sch)
-        assert r.score == 20_000 and r.rescued and not r.overflow
+        r = A.align_pair(kern, 0, q[:2000], q[:20_000], mm(20, -3, 3, 1))
+        assert r.score == 40_000 and r.rescued and not r.overflow
         assert (r.ref_end, r.query_end) == (1999, 1999)
 
 
