@@ -5,6 +5,7 @@
 // and launch on the caller's stream.  No allocation, no synchronisation.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -402,6 +403,14 @@ static ChainGeo chain_geo(int64_t m, int64_t n, int n_sym, int width) {
       best = cost;
       g.li = li; g.L = L; g.nb = (int)(nb < 1 ? 1 : nb);
     }
+  }
+  if (const char* force = getenv("SWB_CHAIN_L")) {  // debugging / tuning override
+    const int L = atoi(force);
+    for (int li = 0; li < 4; ++li)
+      if (Ls[li] == L) {
+        const int64_t rows = 32LL * lpw * L;
+        g.li = li; g.L = L; g.nb = (int)((m + rows - 1) / rows);
+      }
   }
   g.prof_words = (size_t)g.nb * (n_sym + 1) * g.L * 32;
   g.ring_bytes = (size_t)g.nb * kChainRing * kChainK * sizeof(int2);

@@ -149,18 +149,21 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
     // ---- incoming boundary tile ----
     int fin_l = 0, hl_l = 0;
     if (b > 0) {
-      if (t == 0) wait_ge(a.published + (b - 1), (unsigned long long)(t0 + kc));
-      __syncwarp();
+      // every reading lane acquires the producer's release itself
+      wait_ge(a.published + (b - 1), (unsigned long long)(t0 + kc));
       if (t < kc) {
         const int2 v = __ldcg(ring_in + ((t0 + t) % RING));
         fin_l = v.x;
         hl_l = v.y;
       }
       __syncwarp();
-      if (t == 0) st_release(a.consumed + b, (unsigned long long)(t0 + kc));
+      if (t == 0) {
+        __threadfence();
+        st_release(a.consumed + b, (unsigned long long)(t0 + kc));
+      }
     }
-    // ---- back-pressure before producing this tile ----
-    if (b + 1 < nb && t == 0 && t0 >= RING)
+    // ---- back-pressure before producing this tile (the writing lane acquires) ----
+    if (b + 1 < nb && t == T - 1 && t0 >= RING)
       wait_ge(a.consumed + (b + 1), (unsigned long long)(t0 - RING + kc));
     __syncwarp();
     int fo_l = 0, ho_l = 0;  // this tile's outgoing values (lane k holds column t0+k)

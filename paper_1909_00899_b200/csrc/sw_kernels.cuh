@@ -81,9 +81,13 @@ struct W16 {
     return (uint32_t)(lo & 0xffff) | ((uint32_t)hi << 16);
   }
   __device__ static __forceinline__ int hmax(uint32_t v) { return max(get(v, 0), get(v, 1)); }
-  // per-lane (v >= k) as two predicates, one DPX instruction (VIMNMX.S16x2 with predicate out)
+  // per-lane (v >= k) for NON-NEGATIVE lanes (H and column maxima are >= 0).
+  // Deliberately not __vibmax_s16x2: ptxas fuses its max + setp.eq sequence into
+  // a predicate-output VIMNMX.S16x2 whose predicates did not match the intrinsic's
+  // documented (a >= b) semantics in one instance (tools/probes/vibmax_probe.cu).
   __device__ static __forceinline__ void ge2(uint32_t v, uint32_t k, bool& p0, bool& p1) {
-    (void)__vibmax_s16x2(v, k, &p1, &p0);
+    p0 = (v & 0xffffu) >= (k & 0xffffu);
+    p1 = (v & 0xffff0000u) >= (k & 0xffff0000u);
   }
   // shift up by K virtual lanes inside a group of T threads: out[l] = v[l-K], 0 for l < K.
   // `sel` is this thread's PRMT selector for K (identity when t >= K).
