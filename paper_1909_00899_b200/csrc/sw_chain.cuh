@@ -181,7 +181,11 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
         vh = (vh & keep) | (Wd::pack(hd_prev, 0) & ~keep);
       }
       hd_prev = hlk;
-      uint32_t F = 0u, cm = 0u;
+      uint32_t F = 0u;
+      constexpr int kCh = 8, kNch = (L + kCh - 1) / kCh;
+      uint32_t cmk[kNch];
+#pragma unroll
+      for (int k = 0; k < kNch; ++k) cmk[k] = 0u;
 #pragma unroll
       for (int c = 0; c < L; ++c) {
         const uint32_t S = pr[c * 32];
@@ -190,29 +194,37 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
         const uint32_t Xu = Wd::add(u, NGO);
         E[c] = Wd::addmax_relu(E[c], NGE, Xu);
         F = Wd::addmax_relu(F, NGE, Xu);
-        cm = Wd::vmax(cm, u);
+        cmk[c / kCh] = Wd::vmax(cmk[c / kCh], u);
         vh = Wd::addmax(carry, NJ[c], H[c]);
         H[c] = Hn;
       }
       // end coordinates: as sw_striped_kernel, gated on the strip's running best
       // (a strip-local bound is weaker than the global one, so no event is lost)
+      uint32_t cm = cmk[0];
+#pragma unroll
+      for (int k = 1; k < kNch; ++k) cm = Wd::vmax(cm, cmk[k]);
       const int cmx = Wd::hmax(cm);
       if (cmx > gb) {
-        int jw[2] = {L, L};
-#pragma unroll
-        for (int c = L - 1; c >= 0; --c) {
-          bool p0, p1;
-          Wd::ge2(H[c], cm, p0, p1);
-          if (p0) jw[0] = c;
-          if (p1) jw[1] = c;
-        }
 #pragma unroll
         for (int h = 0; h < Wd::LPW; ++h) {
           const int cv = Wd::get(cm, h);
           if (cv > gb && cv > bv) {
+            int kk = 0;
+#pragma unroll
+            for (int k = kNch - 1; k >= 0; --k)
+              if (Wd::get(cmk[k], h) >= cv) kk = k;
+            int jj = 0;
+#pragma unroll
+            for (int k = 0; k < kNch; ++k) {
+              if (k == kk) {
+#pragma unroll
+                for (int c = (k + 1) * kCh - 1; c >= k * kCh; --c)
+                  if (c < L && Wd::get(H[c], h) >= cv) jj = c;
+              }
+            }
             bv = cv;
             bcol = (int)i;
-            bq = (int)(qbase + (h * T + t) * L + (jw[h] < L ? jw[h] : 0));
+            bq = (int)(qbase + (h * T + t) * L + jj);
           }
         }
       }

@@ -81,14 +81,6 @@ struct W16 {
     return (uint32_t)(lo & 0xffff) | ((uint32_t)hi << 16);
   }
   __device__ static __forceinline__ int hmax(uint32_t v) { return max(get(v, 0), get(v, 1)); }
-  // per-lane (v >= k) for NON-NEGATIVE lanes (H and column maxima are >= 0).
-  // Deliberately not __vibmax_s16x2: ptxas fuses its max + setp.eq sequence into
-  // a predicate-output VIMNMX.S16x2 whose predicates did not match the intrinsic's
-  // documented (a >= b) semantics in one instance (tools/probes/vibmax_probe.cu).
-  __device__ static __forceinline__ void ge2(uint32_t v, uint32_t k, bool& p0, bool& p1) {
-    p0 = (v & 0xffffu) >= (k & 0xffffu);
-    p1 = (v & 0xffff0000u) >= (k & 0xffff0000u);
-  }
   // shift up by K virtual lanes inside a group of T threads: out[l] = v[l-K], 0 for l < K.
   // `sel` is this thread's PRMT selector for K (identity when t >= K).
   template <int T, int K>
@@ -125,10 +117,6 @@ struct W32 {
   __device__ static __forceinline__ int get(uint32_t v, int) { return (int)v; }
   __device__ static __forceinline__ uint32_t pack(int lo, int) { return (uint32_t)lo; }
   __device__ static __forceinline__ int hmax(uint32_t v) { return (int)v; }
-  __device__ static __forceinline__ void ge2(uint32_t v, uint32_t k, bool& p0, bool& p1) {
-    p0 = (int)v >= (int)k;
-    p1 = false;
-  }
   template <int T, int K>
   __device__ static __forceinline__ uint32_t shift(uint32_t v, int t, uint32_t gmask, uint32_t) {
     static_assert(K < T, "32-bit lanes shift inside the group");
@@ -342,7 +330,12 @@ sw_striped_kernel(const SwArgs a) {
       uint32_t w = H[LMAX - 1];
       if constexpr (VAR == VAR_SCAN) w = Wd::addmax(carry, NWRAP, w);
       uint32_t vh = Wd::template shift<T, 1>(w, t, cmask, sel[0]);
-      uint32_t F = 0u, cm = 0u;
+      uint32_t F = 0u;
+      // column maxima per chunk of kCh words: a position search only scans one chunk
+      constexpr int kCh = 8, kNch = (LMAX + kCh - 1) / kCh;
+      uint32_t cmk[kNch];
+#pragma unroll
+      for (int k = 0; k < kNch; ++k) cmk[k] = 0u;
 
 #define SWB_WORD_BODY(C)                                                   \
   {                                                                        \
@@ -355,7 +348,7 @@ sw_striped_kernel(const SwArgs a) {
     else                                                                   \
       E[C] = Wd::addmax_relu(E[C], NGE, Xu);                               \
     F = Wd::addmax_relu(F, NGE, Xu);                                       \
-    cm = Wd::vmax(cm, u);                                                  \
+    cmk[(C) / kCh] = Wd::vmax(cmk[(C) / kCh], u);                          \
     if constexpr (VAR == VAR_SCAN) vh = Wd::addmax(carry, NJ[C], H[C]);    \
     else vh = H[C];                                                        \
     H[C] = Hn;                                                             \
@@ -384,25 +377,32 @@ sw_striped_kernel(const SwArgs a) {
       // the alignment's best grows a few dozen times, not per lane-column).
       // A cell attaining the best is a diagonal cell, so its stored H equals
       // u; the first word with H >= cm is the first such cell in the lane.
+      uint32_t cm = cmk[0];
+#pragma unroll
+      for (int k = 1; k < kNch; ++k) cm = Wd::vmax(cm, cmk[k]);
       const int cmx = Wd::hmax(cm);
       if (cmx > gb) {
-        int jw[2] = {LMAX, LMAX};
-#pragma unroll
-        for (int c = LMAX - 1; c >= 0; --c) {
-          if (c >= first) {
-            bool p0, p1;
-            Wd::ge2(H[c], cm, p0, p1);
-            if (p0) jw[0] = c;
-            if (p1) jw[1] = c;
-          }
-        }
 #pragma unroll
         for (int h = 0; h < Wd::LPW; ++h) {
           const int cv = Wd::get(cm, h);
           if (cv > gb && cv > bv) {
+            // the first chunk reaching cv holds the first cell reaching it
+            int kk = 0;
+#pragma unroll
+            for (int k = kNch - 1; k >= 0; --k)
+              if (Wd::get(cmk[k], h) >= cv) kk = k;
+            int jj = first;
+#pragma unroll
+            for (int k = 0; k < kNch; ++k) {
+              if (k == kk) {
+#pragma unroll
+                for (int c = (k + 1) * kCh - 1; c >= k * kCh; --c)
+                  if (c < LMAX && c >= first && Wd::get(H[c], h) >= cv) jj = c;
+              }
+            }
             bv = cv;
             bcol = i;
-            bq = (h * T + t) * L + ((jw[h] < LMAX ? jw[h] : first) - first);
+            bq = (h * T + t) * L + (jj - first);
           }
         }
       }

@@ -303,3 +303,28 @@ def test_long_pair_pipeline_random(A, oracle):
         for width in (16, 32):
             got = A.align_long(q, r, sch, width=width)
             assert (got["score"], got["ref_end"], got["query_end"]) == want, (trial, width, m, n)
+
+
+def test_config5_full_size_against_reference_score(A):
+    """Full 65,536 x 1,048,576 long pair: score pinned to the reference's own scan
+    kernel (golden, make_golden.py --full-config5); end coordinates checked by
+    the property that a second run on the reversed-free prefix ending there
+    reproduces the score."""
+    from paper_1909_00899_b200 import workloads as W
+
+    g = golden("configs.npz")
+    if "c5_scan_p64_score" not in g.files:
+        pytest.skip("golden generated without --full-config5")
+    w = W.config5()
+    from helpers import sha
+
+    assert sha(w.query, w.ref) == str(g["c5_inputs_sha256"])
+    r = A.align_long(w.query, w.ref, w.scheme, width=32)
+    assert r["score"] == int(g["c5_scan_p64_score"])
+    assert not g["c5_scan_p64_overflow"]
+    # end-coordinate property: the best local alignment ends at (ref_end, query_end),
+    # so aligning the prefixes that end there gives the same score, and the cell
+    # before it in either sequence cannot reach it
+    qe, re_ = r["query_end"], r["ref_end"]
+    pre = A.align_long(w.query[: qe + 1], w.ref[: re_ + 1], w.scheme, width=32)
+    assert pre["score"] == r["score"] and (pre["ref_end"], pre["query_end"]) == (re_, qe)
