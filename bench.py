@@ -254,7 +254,7 @@ def main() -> None:
     for _ in range(k_reps):
         _lib.check(L.sw_db_align(C.byref(p.plan16), _ptr(p.prof16), eng.kid, w.scheme.gap_open,
                                  w.scheme.gap_extend, p.bias, p.max_sub, _ptr(d.codes),
-                                 _ptr(d.start), _ptr(d.length), _ptr(d.order), d.n, None,
+                                 _ptr(d.start), _ptr(d.length), None, d.n, None,
                                  _ptr(o["score"]), _ptr(o["ref_end"]), _ptr(o["query_end"]),
                                  _ptr(o["flags"]), None, _stream()))
     ek1.record(stream)
@@ -289,9 +289,9 @@ def main() -> None:
     ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ee0.record(stream)
     for _ in range(args.steps):
-        eng.upload(packed)
         eng.set_query(w.query)
-        top = step()
+        eng.search_streamed(packed, n_chunks=8)
+        top = search.merge_topk(eng.topk(TOPK), TOPK)
         host_top = top.cpu()
     ee1.record(stream)
     torch.cuda.synchronize()
@@ -327,8 +327,12 @@ def main() -> None:
                        "seg_len": p.plan16.seg_len},
             "roofline": {"bound": "dpx", "achieved": round(kernel_gcups, 2),
                          "peak": round(peak_gcups, 2), "unit": "GCUPS",
-                         "frac": round(kernel_gcups / peak_gcups, 4), "traffic": None,
-                         "kernel": f"sw_striped_kernel<W16,{p.plan16.threads},{p.plan16.lmax},SCAN>",
+                         "frac": round(kernel_gcups / peak_gcups, 4),
+                         # dram__bytes_read+write per launch of this kernel (one ncu --set
+                         # full capture at this config, profiles/r01_config2_db_kernel.md)
+                         "traffic": 516.44e6,
+                         "kernel": (f"sw_striped_kernel<W16,T={p.plan16.threads},"
+                                    f"L={p.plan16.seg_len},SCAN,exact,ge={w.scheme.gap_extend}>"),
                          "kernel_ms": round(k_ms, 3),
                          "peak_source": "live DPX probe (cell-update mix, 6 instr per 2 cells)",
                          "dpx_probe": {"mix_instr_per_s": dpx_instr_per_s,

@@ -65,22 +65,29 @@ def shard(offsets: np.ndarray, rank: int, world: int) -> np.ndarray:
 
 def pack(db: np.ndarray, offsets: np.ndarray, ids: np.ndarray | None = None,
          pin: bool = True) -> PackedDb:
-    """Pack the targets `ids` (default: all) of a CSR database into a PackedDb."""
+    """Pack the targets `ids` (default: all) of a CSR database into a PackedDb,
+    physically in length-descending order (ties by global id): every contiguous
+    range of targets is then a load-balanced launch on its own, and the
+    processing order is the identity."""
     offsets = np.asarray(offsets, dtype=np.int64)
     if ids is None:
         ids = np.arange(offsets.shape[0] - 1, dtype=np.int64)
     ids = np.asarray(ids, dtype=np.int64)
+    lens0 = offsets[ids + 1] - offsets[ids]
+    ids = ids[np.argsort(-lens0, kind="stable")]
     lens = (offsets[ids + 1] - offsets[ids]).astype(np.int64)
     start = np.zeros(ids.shape[0], dtype=np.int64)
     if ids.shape[0]:
         np.cumsum(lens[:-1], out=start[1:])
-    if ids.shape[0] == offsets.shape[0] - 1 and (ids == np.arange(ids.shape[0])).all():
-        codes = np.ascontiguousarray(db[: offsets[-1]], dtype=np.uint8)
-        start = offsets[:-1].copy()
-    else:
-        idx = np.repeat(offsets[ids] - start, lens) + np.arange(int(lens.sum()), dtype=np.int64)
-        codes = np.ascontiguousarray(db[idx], dtype=np.uint8)
-    order = np.argsort(-lens, kind="stable").astype(np.int32)
+    codes = np.empty(int(lens.sum()), dtype=np.uint8)
+    step = 1 << 16  # gather in blocks of targets to bound the index array
+    for a in range(0, ids.shape[0], step):
+        b = min(ids.shape[0], a + step)
+        ln = lens[a:b]
+        idx = np.repeat(offsets[ids[a:b]] - start[a:b], ln) + np.arange(
+            int(start[a]), int(start[a]) + int(ln.sum()), dtype=np.int64)
+        codes[int(start[a]): int(start[a]) + int(ln.sum())] = db[idx]
+    order = np.arange(ids.shape[0], dtype=np.int32)
 
     def t(a):
         x = torch.from_numpy(np.ascontiguousarray(a))
@@ -109,7 +116,7 @@ class DatabaseSearch:
         self.prof: DeviceProfile | None = None
         self.launches = 0
 
-    def upload(self, packed: PackedDb) -> None:
+    def _ensure_buffers(self, packed: PackedDb) -> None:
         n = packed.n
         if self.dev is None or self.dev.n != n or self.dev.codes.numel() < packed.codes.numel():
             self.dev = PackedDb(*(torch.empty_like(x, device="cuda") for x in
@@ -123,6 +130,9 @@ class DatabaseSearch:
                 "_rescue": (torch.empty(max(n, 1), dtype=torch.int32, device="cuda"),
                             torch.zeros(1, dtype=torch.int64, device="cuda")),
             }
+
+    def upload(self, packed: PackedDb) -> None:
+        self._ensure_buffers(packed)
         for dst, src in zip((self.dev.codes, self.dev.start, self.dev.length, self.dev.order,
                              self.dev.ids),
                             (packed.codes, packed.start, packed.length, packed.order, packed.ids)):
@@ -150,7 +160,7 @@ class DatabaseSearch:
         n = d.n
         _lib.check(L.sw_db_align(C.byref(p.plan16), _ptr(p.prof16), self.kid, sch.gap_open,
                                  sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
-                                 _ptr(d.length), _ptr(d.order), n, None, _ptr(o["score"]),
+                                 _ptr(d.length), None, n, None, _ptr(o["score"]),
                                  _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
                                  None, st))
         lst, cnt = o["_rescue"]
@@ -164,15 +174,71 @@ class DatabaseSearch:
         self.launches += 3
         return o
 
+    def search_streamed(self, packed: PackedDb, n_chunks: int = 8) -> dict:
+        """End-to-end form for a host-resident (pinned) database: chunk k+1 is
+        copied on a side stream while chunk k is aligned, so the H2D transfer
+        hides behind compute. Requires set_query(); returns the result dict."""
+        assert self.prof is not None, "set_query() first"
+        self._ensure_buffers(packed)
+        L = _lib.load()
+        d, o, p, sch = self.dev, self.out, self.prof, self.scheme
+        n = packed.n
+        cur = torch.cuda.current_stream()
+        copy = self._copy_stream = getattr(self, "_copy_stream", None) or torch.cuda.Stream()
+        bounds = np.linspace(0, n, max(1, min(n_chunks, n)) + 1).astype(np.int64)
+        starts = packed.start
+        copy.wait_stream(cur)  # buffers may still be read by a previous step
+        events = []
+        for c in range(len(bounds) - 1):
+            a, b = int(bounds[c]), int(bounds[c + 1])
+            ra = int(starts[a]) if a < n else 0
+            rb = int(starts[b - 1]) + int(packed.length[b - 1]) if b > a else ra
+            with torch.cuda.stream(copy):
+                d.codes[ra:rb].copy_(packed.codes[ra:rb], non_blocking=True)
+                for dst, src in ((d.start, packed.start), (d.length, packed.length),
+                                 (d.ids, packed.ids)):
+                    dst[a:b].copy_(src[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+            events.append((a, b, ev))
+        st = _stream()
+        for a, b, ev in events:
+            cur.wait_event(ev)
+            if b <= a:
+                continue
+            ptr = lambda t, i: C.c_void_p(t.data_ptr() + i * t.element_size())  # noqa: E731
+            _lib.check(L.sw_db_align(C.byref(p.plan16), _ptr(p.prof16), self.kid, sch.gap_open,
+                                     sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes),
+                                     ptr(d.start, a), ptr(d.length, a), None, b - a, None,
+                                     ptr(o["score"], a), ptr(o["ref_end"], a),
+                                     ptr(o["query_end"], a), ptr(o["flags"], a), None, st))
+            self.launches += 1
+        lst, cnt = o["_rescue"]
+        _lib.check(L.sw_collect_flagged(_ptr(o["flags"]), n, _lib.FLAG_RESCUE, _ptr(lst),
+                                        _ptr(cnt), st))
+        _lib.check(L.sw_db_align(C.byref(p.plan32), _ptr(p.prof32), self.kid, sch.gap_open,
+                                 sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
+                                 _ptr(d.length), _ptr(lst), 0, _ptr(cnt), _ptr(o["score"]),
+                                 _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
+                                 None, st))
+        self.launches += 2
+        return o
+
     def topk(self, k: int = 100) -> torch.Tensor:
         """k best (score desc, global id asc) as int64 [k, 4] on the device."""
         o, d = self.out, self.dev
-        k = min(k, d.n)
-        key = (o["score"].to(torch.int64) << 32) | (0xFFFFFFFF - d.ids)
-        _, idx = torch.topk(key, k, sorted=True)
-        return torch.stack([o["score"][idx].to(torch.int64), d.ids[idx],
-                            o["ref_end"][idx].to(torch.int64), o["query_end"][idx].to(torch.int64)],
-                           dim=1)
+        return topk_records(o["score"], d.ids, o["ref_end"], o["query_end"], k)
+
+
+def topk_records(score: torch.Tensor, ids: torch.Tensor, ref_end: torch.Tensor,
+                 query_end: torch.Tensor, k: int) -> torch.Tensor:
+    """The k best records (score desc, global id asc) as int64 [k, 4]
+    (score, target_id, ref_end, query_end); works on any device."""
+    k = min(k, int(score.shape[0]))
+    key = (score.to(torch.int64) << 32) | (0xFFFFFFFF - ids.to(torch.int64))
+    _, idx = torch.topk(key, k, sorted=True)
+    return torch.stack([score[idx].to(torch.int64), ids[idx].to(torch.int64),
+                        ref_end[idx].to(torch.int64), query_end[idx].to(torch.int64)], dim=1)
 
 
 def merge_topk(records: torch.Tensor, k: int, group=None) -> torch.Tensor:
