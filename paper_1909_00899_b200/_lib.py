@@ -11,7 +11,7 @@ import os
 import subprocess
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libswscan_b200.so")
+LIB_PATH = os.environ.get("SWB_LIB_PATH") or os.path.join(PKG_DIR, "libswscan_b200.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 
 SW_OK, SW_EINVAL, SW_ECUDA, SW_ENOTSUP = 0, -1, -2, -3

@@ -298,7 +298,9 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
   a.query_end = d_query_end;
   a.flags = d_flags;
   a.col_passes = d_col_passes;
-  const size_t smem = (size_t)p->prof_words * 4;
+  // exact instances stage the profile as [sym][ceil(L/4)][T][4]
+  const size_t smem = block == 128 ? (size_t)(p->n_sym + 1) * ((p->seg_len + 3) / 4 * 4) * p->threads * 4
+                                   : (size_t)p->prof_words * 4;
   const int G = 32 / p->threads;
   const int64_t tasks = d_n_jobs ? 0 : (n + G - 1) / G;
   return launch(fn, a, smem, block, tasks, (cudaStream_t)stream);
@@ -370,10 +372,12 @@ int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8
   a.query_end = d_query_end;
   a.flags = d_flags;
   a.col_passes = d_col_passes;
-  a.pair_stride = (n_sym + 1) * p.seg_len * p.threads;
+  const bool vec = max_block == 128;  // exact instance: vectorised profile layout
+  const int lslice = vec ? (p.seg_len + 3) / 4 * 4 : p.seg_len;
+  a.pair_stride = (n_sym + 1) * lslice * p.threads;
   // block size: as many warps as the per-group profile slices allow (<= 256 threads)
   int block = max_block;
-  const size_t per_thread = (size_t)(n_sym + 1) * p.seg_len * 4;  // slice bytes / T
+  const size_t per_thread = (size_t)(n_sym + 1) * lslice * 4;  // slice bytes / T
   while (block > 32 && per_thread * block > 110 * 1024) block >>= 1;
   const size_t smem = per_thread * block;
   if (smem > 227 * 1024) return fail(SW_ENOTSUP, "pair profile slice too large (%zu B)", smem);

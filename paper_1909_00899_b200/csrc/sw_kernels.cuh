@@ -58,6 +58,10 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return r;
 }
 
+__device__ __forceinline__ uint32_t w4(const uint4& v, int k) {
+  return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+}
+
 // ---- word policies -------------------------------------------------------
 struct W16 {
   static constexpr int LPW = 2;
@@ -182,8 +186,17 @@ struct SwArgs {
   X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29)  \
   X(30) X(31)
 
+#ifndef SWB_EXACT_MINB
+#define SWB_EXACT_MINB 3  // CTAs of 128 threads per SM the exact kernels are register-capped for
+#endif
+#ifndef SWB_COL_UNROLL
+#define SWB_COL_UNROLL 1  // reference columns per loop iteration (unroll factor)
+#endif
+#define SWB_PRAGMA(x) _Pragma(#x)
+#define SWB_UNROLL(n) SWB_PRAGMA(unroll n)
+
 template <class Wd, int T, int LMAX, int VAR, bool EXACT = false, int GE = 0>
-__global__ void __launch_bounds__(EXACT ? 128 : 256, EXACT ? 4 : 1)
+__global__ void __launch_bounds__(EXACT ? 128 : 256, EXACT ? SWB_EXACT_MINB : 1)
 sw_striped_kernel(const SwArgs a) {
   // GE > 0: gap-extend penalty known at compile time, so every decay constant
   // (j*ge, k*L*ge) is an immediate operand of VIADDMNMX instead of a register.
@@ -195,6 +208,8 @@ sw_striped_kernel(const SwArgs a) {
   constexpr int P = Geo<Wd, T>::P;
   constexpr int STEPS = Geo<Wd, T>::STEPS;
   constexpr int G = 32 / T;
+  constexpr bool VEC = EXACT;          // vectorised [sym][L/4][T][4] profile layout
+  constexpr int LP4 = (LMAX + 3) / 4;
 
   extern __shared__ uint32_t smem[];
 
@@ -246,14 +261,27 @@ sw_striped_kernel(const SwArgs a) {
     m = a.shared_m;
     first = LMAX - L;
     LT = L * T;
-    const int words = (A + 1) * LT;
-    const uint4* src = reinterpret_cast<const uint4*>(a.prof);
-    uint4* dst = reinterpret_cast<uint4*>(smem);
-    for (int w = threadIdx.x; w < (words >> 2); w += blockDim.x) dst[w] = __ldg(src + w);
-    for (int w = (words & ~3) + threadIdx.x; w < words; w += blockDim.x) smem[w] = __ldg(a.prof + w);
+    if constexpr (VEC) {
+      // [(A+1)][L/4][T][4]: a thread's 4 consecutive words are one 16-byte LDS and
+      // a group (quarter warp) reads 128 contiguous bytes: no bank conflicts
+      // between the groups of a warp, which read different symbol rows.
+      const int words = (A + 1) * LP4 * T * 4;
+      for (int w = threadIdx.x; w < words; w += blockDim.x) {
+        const int k = w & 3, tt = (w >> 2) % T, j4 = (w / (4 * T)) % LP4, sym = w / (4 * T * LP4);
+        const int j = 4 * j4 + k;
+        smem[w] = j < L ? __ldg(a.prof + (sym * L + j) * T + tt) : 0u;
+      }
+      LT = LP4 * T * 4;
+    } else {
+      const int words = (A + 1) * LT;
+      const uint4* src = reinterpret_cast<const uint4*>(a.prof);
+      uint4* dst = reinterpret_cast<uint4*>(smem);
+      for (int w = threadIdx.x; w < (words >> 2); w += blockDim.x) dst[w] = __ldg(src + w);
+      for (int w = (words & ~3) + threadIdx.x; w < words; w += blockDim.x) smem[w] = __ldg(a.prof + w);
+    }
     __syncthreads();
     set_gaps(a.go, a.ge, L);
-    prof_base = smem + t - first * T;
+    prof_base = VEC ? smem + 4 * t : smem + t - first * T;
   } else {
     LT = 0;
     prof_base = nullptr;
@@ -300,10 +328,14 @@ sw_striped_kernel(const SwArgs a) {
             }
             v[h] = s;
           }
-          gslice[(sym * L + j) * T + t] = Wd::pack(v[0], v[1]);
+          if constexpr (VEC)
+            gslice[((sym * LP4 + (j >> 2)) * T + t) * 4 + (j & 3)] = Wd::pack(v[0], v[1]);
+          else
+            gslice[(sym * L + j) * T + t] = Wd::pack(v[0], v[1]);
         }
       }
-      prof_base = gslice + t - first * T;
+      if constexpr (VEC) LT = LP4 * T * 4;
+      prof_base = VEC ? gslice + 4 * t : gslice + t - first * T;
     }
     const int maxlen = __reduce_max_sync(0xffffffffu, len);
 
@@ -317,10 +349,16 @@ sw_striped_kernel(const SwArgs a) {
     const int nullsym = A;
     int nxt = (len > 0) ? (int)__ldg(tp) : nullsym;
 
+    SWB_UNROLL(SWB_COL_UNROLL)
     for (int i = 0; i < maxlen; ++i) {
       const int sym = nxt;
       nxt = (i + 1 < len) ? (int)__ldg(tp + i + 1) : nullsym;
       const uint32_t* pr = prof_base + sym * LT;
+      uint4 S4[VEC ? LP4 : 1];
+      if constexpr (VEC) {
+#pragma unroll
+        for (int k = 0; k < LP4; ++k) S4[k] = *reinterpret_cast<const uint4*>(pr + k * T * 4);
+      }
 
       // scan path: the whole warp is converged here, so shuffles take the full
       // mask (width T keeps the data inside the group) and skip the runtime
@@ -339,7 +377,7 @@ sw_striped_kernel(const SwArgs a) {
 
 #define SWB_WORD_BODY(C)                                                   \
   {                                                                        \
-    const uint32_t S = pr[(C) * T];                                        \
+    const uint32_t S = VEC ? w4(S4[VEC ? (C) / 4 : 0], (C) & 3) : pr[(C) * T]; \
     const uint32_t u = Wd::addmax(vh, S, E[C]);                            \
     const uint32_t Hn = Wd::vmax(u, F);                                    \
     const uint32_t Xu = Wd::add(u, NGO);                                   \
