@@ -328,3 +328,79 @@ def test_config5_full_size_against_reference_score(A):
     qe, re_ = r["query_end"], r["ref_end"]
     pre = A.align_long(w.query[: qe + 1], w.ref[: re_ + 1], w.scheme, width=32)
     assert pre["score"] == r["score"] and (pre["ref_end"], pre["query_end"]) == (re_, qe)
+
+
+# ---- full-size properties (BASELINE sizes) ---------------------------------------------
+
+
+def test_config2_full_database_properties(A, oracle):
+    """1,000,000 targets: scan == lazy-F (16-bit) == scan (32-bit) on every target;
+    400 seeded random targets against the scalar oracle (scores + end coordinates)."""
+    import torch as T
+
+    from paper_1909_00899_b200 import search, workloads as W
+
+    w = W.config2()
+    packed = search.pack(w.db, w.offsets, pin=False)
+    res = {}
+    for kern in ("scan", "lazyf"):
+        eng = search.DatabaseSearch(w.scheme, kernel=kern)
+        eng.upload(packed)
+        eng.set_query(w.query)
+        o = eng.align()
+        ids = eng.dev.ids.cpu().numpy()
+        order = np.argsort(ids)
+        res[kern] = {k: o[k].cpu().numpy()[order] for k in ("score", "ref_end", "query_end")}
+    for k in ("score", "ref_end", "query_end"):
+        assert (res["scan"][k] == res["lazyf"][k]).all(), k
+    # 32-bit scan over the same targets
+    prof = A.build_profile_arrays(w.query, w.scheme)
+    prof.ensure32()
+    tgt = T.from_numpy(w.db).cuda()
+    start = T.from_numpy(w.offsets[:-1].copy()).cuda()
+    length = T.from_numpy(np.diff(w.offsets).astype(np.int32)).cuda()
+    import ctypes as C
+
+    from paper_1909_00899_b200 import _lib
+    from paper_1909_00899_b200.align import _ptr, _stream
+
+    n = w.n_targets
+    o32 = {k: T.empty(n, dtype=T.int32, device="cuda") for k in ("score", "ref_end", "query_end")}
+    fl = T.empty(n, dtype=T.uint8, device="cuda")
+    _lib.check(_lib.load().sw_db_align(C.byref(prof.plan32), _ptr(prof.prof32), 2, 11, 1,
+                                       prof.bias, prof.max_sub, _ptr(tgt), _ptr(start),
+                                       _ptr(length), None, n, None, _ptr(o32["score"]),
+                                       _ptr(o32["ref_end"]), _ptr(o32["query_end"]), _ptr(fl),
+                                       None, _stream()))
+    for k in ("score", "ref_end", "query_end"):
+        assert (o32[k].cpu().numpy() == res["scan"][k]).all(), k
+    rng = np.random.default_rng(0xD0B)
+    pick = np.sort(rng.choice(n, 400, replace=False))
+    sub_off = np.concatenate([[0], np.cumsum(np.diff(w.offsets)[pick])]).astype(np.int64)
+    sub_db = np.concatenate([w.db[w.offsets[i]:w.offsets[i + 1]] for i in pick])
+    sc, re_, qe = oracle.db_scalar(w.query, sub_db, sub_off, w.scheme.as_array(), 11, 1)
+    assert (res["scan"]["score"][pick] == sc).all()
+    assert (res["scan"]["ref_end"][pick] == re_).all()
+    assert (res["scan"]["query_end"][pick] == qe).all()
+
+
+def test_config3_large_batch_properties(A, oracle):
+    """2^20 short-read pairs (1/16 of config 3): scan == lazy-F everywhere, every
+    planted read aligns, 500 seeded random pairs against the scalar oracle."""
+    from paper_1909_00899_b200 import workloads as W
+
+    w = W.config3(n_pairs=1 << 20)
+    r1 = A.pairs_align(w.flat_q, w.q_off, w.flat_r, w.r_off, kernel="scan", scheme=w.scheme)
+    r2 = A.pairs_align(w.flat_q, w.q_off, w.flat_r, w.r_off, kernel="lazyf", scheme=w.scheme)
+    for k in ("score", "ref_end", "query_end"):
+        assert (r1[k] == r2[k]).all(), k
+    assert np.median(r1["score"]) > 200  # reads are planted copies (150 nt, +2 per match)
+    rng = np.random.default_rng(0x3EAD)
+    pick = np.sort(rng.choice(w.n_pairs, 500, replace=False))
+    fq = np.concatenate([w.flat_q[w.q_off[i]:w.q_off[i + 1]] for i in pick])
+    fr = np.concatenate([w.flat_r[w.r_off[i]:w.r_off[i + 1]] for i in pick])
+    qo = np.arange(501, dtype=np.int64) * 150
+    ro = np.arange(501, dtype=np.int64) * 300
+    sc, re_, qe = oracle.batch_scalar(fq, qo, fr, ro, sub=w.scheme.as_array(), go=6, ge=1)
+    assert (r1["score"][pick] == sc).all()
+    assert (r1["ref_end"][pick] == re_).all() and (r1["query_end"][pick] == qe).all()
