@@ -419,7 +419,7 @@ static ChainGeo chain_geo(int64_t m, int64_t n, int n_sym, int width) {
   g.prof_words = (size_t)g.nb * (n_sym + 1) * g.L * 32;
   g.ring_bytes = (size_t)g.nb * kChainRing * kChainK * sizeof(int2);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  g.total = al(g.prof_words * 4) + al(g.ring_bytes) + al(g.nb * 8) * 2 + al(g.nb * 16) + 256;
+  g.total = al(g.prof_words * 4) + al(g.ring_bytes) + al(g.nb * 128) * 2 + al(g.nb * 16) + 256;
   return g;
 }
 
@@ -453,10 +453,10 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
   int2* ring = (int2*)ws;
   ws += al(g.ring_bytes);
   char* zero_begin = ws;
-  unsigned long long* published = (unsigned long long*)ws;
-  ws += al(g.nb * 8);
+  unsigned long long* published = (unsigned long long*)ws;  // one 128-B line per strip
+  ws += al(g.nb * 128);
   unsigned long long* consumed = (unsigned long long*)ws;
-  ws += al(g.nb * 8);
+  ws += al(g.nb * 128);
   int4* best = (int4*)ws;
   ws += al(g.nb * 16);
   unsigned int* done = (unsigned int*)ws;
@@ -492,6 +492,11 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
   a.ref_end = d_ref_end;
   a.query_end = d_query_end;
   a.flags = d_flags;
+  if (const char* tp = getenv("SWB_CHAIN_TRACE_PTR")) {  // diagnostics timeline
+    a.trace = (unsigned long long*)strtoull(tp, nullptr, 0);
+    a.trace_tiles = atoi(getenv("SWB_CHAIN_TRACE_TILES"));
+    a.reverse = getenv("SWB_CHAIN_REVERSE") != nullptr;
+  }
   const void* fn = g_chain[wi][g.li];
   const size_t smem = (size_t)(n_sym + 1) * g.L * 32 * 4;
   if (smem > 48 * 1024) {

@@ -21,6 +21,18 @@
 
 namespace swb {
 
+#ifndef SWB_CHAIN_COORDS
+#define SWB_CHAIN_COORDS 1
+#endif
+#ifndef SWB_CHAIN_SLEEP
+#define SWB_CHAIN_SLEEP 1
+#endif
+#ifndef SWB_CHAIN_BP_ALL
+// Back-pressure spin by every lane.  With only the writing lane spinning (divergent),
+// the head strip's warp stayed in a degraded issue mode afterwards: ~9x slower columns
+// for the rest of the kernel (measured with tools/trace_chain.py).
+#define SWB_CHAIN_BP_ALL 1
+#endif
 constexpr int kChainK = 32;     // columns per handoff tile
 constexpr int kChainRing = 8;   // tiles in flight per boundary
 
@@ -35,8 +47,8 @@ struct ChainArgs {
   int32_t early_exit;
   // workspace (zeroed before launch)
   int2* ring;                     // [nb][kChainRing*kChainK] (F_out, H_last)
-  unsigned long long* published;  // [nb] columns published by strip b
-  unsigned long long* consumed;   // [nb] columns consumed by strip b (from strip b-1)
+  unsigned long long* published;  // [nb*16] columns published by strip b (one 128-B line each)
+  unsigned long long* consumed;   // [nb*16] columns consumed by strip b (from strip b-1)
   int4* best;                     // [nb] per-strip (score, col, q, 0)
   unsigned int* done;             // [1] ticket
   // outputs
@@ -44,7 +56,17 @@ struct ChainArgs {
   int32_t* ref_end;
   int32_t* query_end;
   uint8_t* flags;
+  // optional timeline (diagnostics): per strip, per tile: [start, ready, end] globaltimer ns
+  unsigned long long* trace;
+  int32_t trace_tiles;
+  int32_t reverse;  // diagnostics: strip b runs on block nb-1-b
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+  return v;
+}
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
@@ -55,13 +77,23 @@ __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long 
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Spin with relaxed loads (an acquire load per iteration would invalidate L1 every
+// poll), then one acquire fence once the producer's release is observed.
 __device__ __forceinline__ void wait_ge(const unsigned long long* p, unsigned long long want) {
-  if (ld_acquire(p) >= want) return;
-  unsigned ns = 32;
-  while (ld_acquire(p) < want) {
-    __nanosleep(ns);
-    if (ns < 1024) ns <<= 1;
+  if (ld_relaxed(p) < want) {
+    unsigned ns = 32;
+    while (ld_relaxed(p) < want) {
+      if (SWB_CHAIN_SLEEP) __nanosleep(ns);
+      if (ns < 512) ns <<= 1;
+    }
   }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
 // Chain profile: strip-major layout prof[b][(A+1)][L][32] so each CTA reads one contiguous slab.
@@ -96,7 +128,7 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
   constexpr int STEPS = ceil_log2(P);
   constexpr int RING = kChainRing * kChainK;
   const int t = threadIdx.x;
-  const int b = blockIdx.x;
+  const int b = a.reverse ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;
   const int nb = a.nb;
   const uint32_t gmask = 0xffffffffu;
   const int A = a.n_sym;
@@ -110,6 +142,11 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
     __syncwarp();
   }
   const uint32_t* prof_t = smem + t;
+  if (a.trace && t == 0) {  // diagnostics: SM of this strip, after the timeline
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    a.trace[(size_t)64 * a.trace_tiles * 4 + b] = smid;  // tools/trace_chain.py reserves 64 strips
+  }
 
   uint32_t sel[6];
 #pragma unroll
@@ -146,31 +183,37 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
 
   for (int64_t t0 = 0; t0 < n; t0 += kChainK) {
     const int kc = (int)min((int64_t)kChainK, n - t0);
+    const int64_t tile = t0 / kChainK;
+    unsigned long long* tr = (a.trace && tile < a.trace_tiles && t == 0)
+                                 ? a.trace + ((size_t)b * a.trace_tiles + tile) * 4 : nullptr;
+    unsigned long long* tr31 = (a.trace && tile < a.trace_tiles && t == T - 1)
+                                   ? a.trace + ((size_t)b * a.trace_tiles + tile) * 4 : nullptr;
+    if (tr) tr[0] = gtimer();
     // ---- incoming boundary tile ----
     int fin_l = 0, hl_l = 0;
     if (b > 0) {
       // every reading lane acquires the producer's release itself
-      wait_ge(a.published + (b - 1), (unsigned long long)(t0 + kc));
+      wait_ge(a.published + (size_t)(b - 1) * 16, (unsigned long long)(t0 + kc));
       if (t < kc) {
         const int2 v = __ldcg(ring_in + ((t0 + t) % RING));
         fin_l = v.x;
         hl_l = v.y;
       }
       __syncwarp();
-      if (t == 0) {
-        __threadfence();
-        st_release(a.consumed + b, (unsigned long long)(t0 + kc));
-      }
+      if (t == 0) st_release(a.consumed + (size_t)b * 16, (unsigned long long)(t0 + kc));
     }
     // ---- back-pressure before producing this tile (the writing lane acquires) ----
-    if (b + 1 < nb && t == T - 1 && t0 >= RING)
-      wait_ge(a.consumed + (b + 1), (unsigned long long)(t0 - RING + kc));
+    if (b + 1 < nb && (SWB_CHAIN_BP_ALL || t == T - 1) && t0 >= RING)
+      wait_ge(a.consumed + (size_t)(b + 1) * 16, (unsigned long long)(t0 - RING + kc));
+    if (tr31) tr31[3] = gtimer();
     __syncwarp();
+    if (tr) tr[1] = gtimer();
     int fo_l = 0, ho_l = 0;  // this tile's outgoing values (lane k holds column t0+k)
+    const int sym_l = t < kc ? (int)__ldg(a.ref + t0 + t) : 0;  // lane k: residue of column t0+k
 
     for (int k = 0; k < kc; ++k) {
       const int64_t i = t0 + k;
-      const int sym = (int)__ldg(a.ref + i);
+      const int sym = __shfl_sync(gmask, sym_l, k);
       const uint32_t* pr = prof_t + sym * (L * 32);
       const int fin = __shfl_sync(gmask, fin_l, k);
       const int hlk = __shfl_sync(gmask, hl_l, k);
@@ -204,7 +247,7 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
 #pragma unroll
       for (int k = 1; k < kNch; ++k) cm = Wd::vmax(cm, cmk[k]);
       const int cmx = Wd::hmax(cm);
-      if (cmx > gb) {
+      if (SWB_CHAIN_COORDS && cmx > gb) {
 #pragma unroll
         for (int h = 0; h < Wd::LPW; ++h) {
           const int cv = Wd::get(cm, h);
@@ -250,21 +293,18 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
       carry = Wd::addmax(Wd::splat(fin), NLANE, acc);
       wnext = Wd::addmax(carry, NWRAP, H[L - 1]);       // corrected H of the last word
       const uint32_t fo = Wd::addmax(carry, NLD, F);    // true F leaving each lane
-      if (t == T - 1) {
-        fo_l = Wd::get(fo, Wd::LPW - 1);
-        ho_l = Wd::get(wnext, Wd::LPW - 1);
-        if (b + 1 < nb) ring_out[i % RING] = make_int2(fo_l, ho_l);
-      }
+      // the strip's last lane (thread 31, top half) holds this column's boundary
+      // pair; park it in lane k so the tile leaves in one coalesced store
+      const int fo_k = __shfl_sync(gmask, Wd::get(fo, Wd::LPW - 1), T - 1);
+      const int ho_k = __shfl_sync(gmask, Wd::get(wnext, Wd::LPW - 1), T - 1);
+      if (t == k) { fo_l = fo_k; ho_l = ho_k; }
     }
     if (b + 1 < nb) {
+      if (t < kc) ring_out[(t0 + t) % RING] = make_int2(fo_l, ho_l);
       __syncwarp();
-      if (t == T - 1) {
-        __threadfence();
-        st_release(a.published + b, (unsigned long long)(t0 + kc));
-      }
+      if (t == 0) st_release(a.published + (size_t)b * 16, (unsigned long long)(t0 + kc));
     }
-    (void)fo_l;
-    (void)ho_l;
+    if (tr) tr[2] = gtimer();
   }
 
   // ---- per-strip best, then the last strip to finish reduces ----
