@@ -187,9 +187,16 @@ def main() -> None:
     from paper_1909_00899_b200 import _lib, search, workloads as W
 
     world, rank, local = dist_env()
-    torch.cuda.set_device(local)
+    # SWB_DIST_BACKEND=gloo lets the multi-rank path run with several ranks on one
+    # GPU (shards never wait on each other); the product path is NCCL, one rank per GPU.
+    backend = os.environ.get("SWB_DIST_BACKEND", "nccl")
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local % ndev))
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
@@ -235,7 +242,7 @@ def main() -> None:
     ms = ev0.elapsed_time(ev1)
     gpu_launches = eng.launches - launches0
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
@@ -302,7 +309,7 @@ def main() -> None:
     torch.cuda.synchronize()
     e2e_ms = ee0.elapsed_time(ee1)
     if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
+        t = torch.tensor([e2e_ms], device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_value = total_cells / (e2e_ms / args.steps * 1e-3) / 1e9

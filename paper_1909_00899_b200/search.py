@@ -248,6 +248,9 @@ def merge_topk(records: torch.Tensor, k: int, group=None) -> torch.Tensor:
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return records
     world = dist.get_world_size(group)
+    dev = records.device
+    if dist.get_backend(group) == "gloo":  # gloo collectives run on host tensors
+        records = records.cpu()
     kk = torch.full((k, 4), -1, dtype=torch.int64, device=records.device)
     kk[: records.shape[0]] = records
     kk[records.shape[0]:, 0] = -1  # padding (scores are >= 0) loses every comparison
@@ -256,4 +259,4 @@ def merge_topk(records: torch.Tensor, k: int, group=None) -> torch.Tensor:
     allr = torch.cat(gathered)
     key = (allr[:, 0] << 32) | (0xFFFFFFFF - (allr[:, 1] & 0xFFFFFFFF))
     _, idx = torch.topk(key, min(k, allr.shape[0]), sorted=True)
-    return allr[idx]
+    return allr[idx].to(dev)
