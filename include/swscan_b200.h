@@ -84,14 +84,17 @@ int32_t sw_profile_build(const sw_plan_t* plan, const uint8_t* d_query, const in
  * (length-sorted, descending, for load balance).  d_n_jobs (nullable): device
  * job count overriding n: a rescue pass that runs without a host sync; its
  * results are marked SW_FLAG_RESCUED.
- * Outputs are indexed by job id; d_ref_end/d_query_end/d_flags/d_col_passes nullable.
- * d_col_passes (lazy-F kernels): per-column correction passes of job 0. */
+ * Outputs are indexed by job id; d_ref_end/d_query_end/d_flags/d_col_passes/d_pass_stats
+ * nullable.  d_col_passes (lazy-F kernels): per-column correction passes of job 0.
+ * d_pass_stats (lazy-F kernels): int64 [n][2] = (total correction passes, columns that
+ * took the early exit) per alignment -- with the reference layout and a *_MIRROR
+ * kernel these reproduce the reference's OpCounters exactly (src/vectors.py:61-95). */
 int32_t sw_db_align(const sw_plan_t* plan, const uint32_t* d_prof, int32_t kernel,
                     int32_t gap_open, int32_t gap_extend, int32_t bias, int32_t max_sub,
                     const uint8_t* d_tgt, const int64_t* d_start, const int32_t* d_len,
                     const int32_t* d_order, int64_t n, const int64_t* d_n_jobs,
                     int32_t* d_score, int32_t* d_ref_end, int32_t* d_query_end, uint8_t* d_flags,
-                    int32_t* d_col_passes, sw_stream_t stream);
+                    int32_t* d_col_passes, int64_t* d_pass_stats, sw_stream_t stream);
 
 /* n independent (query_k, target_k) pairs.  Reference: batch_align(kernel_id, p,
  * flat_q, q_off, flat_r, r_off, match_a, mis_a, go_a, ge_a), src/_compiled.py:504-529.
@@ -108,7 +111,7 @@ int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8
                        int32_t max_sub, const int32_t* d_match, const int32_t* d_mismatch,
                        const int32_t* d_go, const int32_t* d_ge, int32_t* d_score,
                        int32_t* d_ref_end, int32_t* d_query_end, uint8_t* d_flags,
-                       int32_t* d_col_passes, sw_stream_t stream);
+                       int32_t* d_col_passes, int64_t* d_pass_stats, sw_stream_t stream);
 
 /* Long single pairs (query beyond the warp kernels' 2048 16-bit / 1024 32-bit
  * positions, e.g. config 4/5): a pipeline of query strips, one warp-sized CTA

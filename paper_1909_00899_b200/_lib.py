@@ -104,10 +104,10 @@ def load():
     L.sw_profile_build.argtypes = [C.POINTER(Plan), vp, vp, i32, vp, vp]
     L.sw_db_align.restype = i32
     L.sw_db_align.argtypes = [C.POINTER(Plan), vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, i64,
-                              vp, vp, vp, vp, vp, vp, vp]
+                              vp, vp, vp, vp, vp, vp, vp, vp]
     L.sw_pairs_align.restype = i32
     L.sw_pairs_align.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, vp, i32, i32, vp, i32,
-                                 i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+                                 i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.sw_collect_flagged.restype = i32
     L.sw_collect_flagged.argtypes = [vp, i64, C.c_uint8, vp, vp, vp]
     L.sw_scan_lanes.restype = i32

@@ -261,7 +261,7 @@ def db_align(prof: DeviceProfile, tgt: torch.Tensor, start: torch.Tensor, length
                              sch.gap_extend, prof.bias, prof.max_sub, _ptr(tgt), _ptr(start),
                              _ptr(length), _ptr(order), n, None, _ptr(out["score"]),
                              _ptr(out["ref_end"]), _ptr(out["query_end"]), _ptr(out["flags"]),
-                             _ptr(col_passes), st))
+                             _ptr(col_passes), None, st))
     if rescue:
         _rescue_db(prof, tgt, start, length, kid, col_passes, out, n)
     return out
@@ -283,7 +283,7 @@ def _rescue_db(prof, tgt, start, length, kid, col_passes, out, n) -> None:
                              sch.gap_extend, prof.bias, prof.max_sub, _ptr(tgt), _ptr(start),
                              _ptr(length), _ptr(ws[0]), 0, _ptr(ws[1]), _ptr(out["score"]),
                              _ptr(out["ref_end"]), _ptr(out["query_end"]), _ptr(out["flags"]),
-                             _ptr(col_passes), st))
+                             _ptr(col_passes), None, st))
 
 
 def _result_from(prof_or_none, kernel, n, L_, P, score, flags, rend, qend, passes) -> AlignmentResult:
@@ -370,14 +370,34 @@ def scalar_score(query, ref, scheme: ScoringScheme) -> int:
     return align_pair("scan", 0, q, r, scheme).score
 
 
+def counters_from_stats(kernel: str, n: int, L: int, p: int, total_passes: int,
+                        breaks: int) -> list[int]:
+    """Reference op counters (src/_compiled.py:137-219, :246-339) of one alignment
+    from its column count n, layout (L, p) and device pass statistics."""
+    if n <= 0:
+        return [0] * 7
+    if kernel == "scan":
+        c = counters_from_passes("scan", n, L, p, np.zeros(0))
+    else:
+        k = int(total_passes)
+        c = OpCounters(shifts=n + k + int(breaks), sat_adds=n * L, sat_subs=n * 4 * L + k * L,
+                       maxes=n * 5 * L + k * L, loads=n * (1 + 3 * L) + k * L,
+                       stores=n * 2 * L + k * L, correction_passes=k)
+    return [c.shifts, c.sat_adds, c.sat_subs, c.maxes, c.loads, c.stores, c.correction_passes]
+
+
 def pairs_align(flat_q, q_off, flat_r, r_off, *, kernel: str = "scan", lanes: int = 0,
                 scheme: ScoringScheme | None = None, match_a=None, mis_a=None, go_a=None,
-                ge_a=None, width: int = 16) -> dict:
-    """Independent pairs (CSR queries/targets), device-resident results.
+                ge_a=None, width: int = 16, stats: bool = False) -> dict:
+    """Independent pairs (CSR queries/targets), results as numpy arrays
+    ``score, ref_end, query_end, flags`` (+ ``pass_stats``, ``lanes_used``,
+    ``seg_len`` with ``stats=True``).
 
     Scoring is either one shared ``scheme`` or per-pair 4x4 match/mismatch
     schemes like the reference's batch_align (src/_compiled.py:504-529).
-    Returns numpy arrays ``score, ref_end, query_end, flags``."""
+    ``lanes = p`` runs every pair whose segment ``ceil(m/p)`` fits the register
+    budget in the reference layout (exact pass counts); the rest run in the
+    throughput layout (identical scores and end coordinates)."""
     _require_cuda()
     L = _lib.load()
     q_off = np.asarray(q_off, dtype=np.int64)
@@ -388,12 +408,12 @@ def pairs_align(flat_q, q_off, flat_r, r_off, *, kernel: str = "scan", lanes: in
     fr = _codes(flat_r, n_sym, "reference")
     qlen = np.diff(q_off).astype(np.int32)
     tlen = np.diff(r_off).astype(np.int32)
+    res = {"score": np.zeros(n, np.int64), "ref_end": np.full(n, -1, np.int32),
+           "query_end": np.full(n, -1, np.int32), "flags": np.zeros(n, np.uint8),
+           "pass_stats": np.zeros((n, 2), np.int64), "lanes_used": np.zeros(n, np.int32),
+           "seg_len": np.zeros(n, np.int32)}
     if n == 0:
-        z = np.zeros(0, np.int64)
-        return {"score": z, "ref_end": z.astype(np.int32), "query_end": z.astype(np.int32),
-                "flags": z.astype(np.uint8)}
-    # process pairs grouped by query length (segment length uniform per warp)
-    order = np.lexsort((-tlen, -qlen)).astype(np.int32)
+        return res
     dev = {
         "qry": torch.from_numpy(fq if fq.size else np.zeros(1, np.uint8)).cuda(),
         "qs": torch.from_numpy(q_off[:-1].copy()).cuda(),
@@ -401,7 +421,6 @@ def pairs_align(flat_q, q_off, flat_r, r_off, *, kernel: str = "scan", lanes: in
         "tgt": torch.from_numpy(fr if fr.size else np.zeros(1, np.uint8)).cuda(),
         "ts": torch.from_numpy(r_off[:-1].copy()).cuda(),
         "tl": torch.from_numpy(tlen).cuda(),
-        "order": torch.from_numpy(order).cuda(),
     }
     per_pair = scheme is None
     if per_pair:
@@ -412,51 +431,98 @@ def pairs_align(flat_q, q_off, flat_r, r_off, *, kernel: str = "scan", lanes: in
         pp = [None] * 4
         sub_t = torch.from_numpy(scheme.as_array()).cuda()
         go, ge, bias, max_sub = scheme.gap_open, scheme.gap_extend, scheme.bias, scheme.max_score
-    out = {k: torch.empty(n, dtype=torch.int32, device="cuda")
+    out = {k: torch.zeros(n, dtype=torch.int32, device="cuda")
            for k in ("score", "ref_end", "query_end")}
-    out["flags"] = torch.empty(n, dtype=torch.uint8, device="cuda")
-    max_q = int(qlen.max()) if n else 0
-    min_q = int(qlen.min()) if n else 0
+    out["flags"] = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    pstats = torch.zeros((n, 2), dtype=torch.int64, device="cuda") if stats else None
     kid = _kernel_id(kernel)
     st = _stream()
 
-    def run(width_, lanes_, order_, n_, n_dev):
+    def run(width_, lanes_, order_np, n_dev=None, max_q=None, min_q=None):
+        order_t = torch.from_numpy(order_np.astype(np.int32)).cuda()
+        n_ = 0 if n_dev is not None else int(order_np.shape[0])
         _lib.check(L.sw_pairs_align(width_, lanes_, kid, _ptr(dev["qry"]), _ptr(dev["qs"]),
                                     _ptr(dev["ql"]), _ptr(dev["tgt"]), _ptr(dev["ts"]),
-                                    _ptr(dev["tl"]), _ptr(order_), n_, _ptr(n_dev), min_q, max_q,
-                                    _ptr(sub_t), n_sym, go, ge, bias, max_sub, *[_ptr(x) for x in pp],
-                                    _ptr(out["score"]), _ptr(out["ref_end"]),
-                                    _ptr(out["query_end"]), _ptr(out["flags"]), None, st))
+                                    _ptr(dev["tl"]), _ptr(order_t), n_, _ptr(n_dev), min_q, max_q,
+                                    _ptr(sub_t), n_sym, go, ge, bias, max_sub,
+                                    *[_ptr(x) for x in pp], _ptr(out["score"]),
+                                    _ptr(out["ref_end"]), _ptr(out["query_end"]),
+                                    _ptr(out["flags"]), None, _ptr(pstats), st))
+        return order_t
 
-    lanes_eff = lanes
+    # partition: reference layout where it fits, throughput layout elsewhere
+    groups = []
     if lanes:
+        Lp = (qlen.astype(np.int64) + lanes - 1) // lanes
+        fits = np.zeros(n, bool)
         try:
-            _lib.plan_query(max_q, n_sym, width, lanes)
+            _lib.plan_query(1, n_sym, width, lanes)
+            fits = Lp <= 32
         except _lib.SwError:
-            lanes_eff = 0
-    run(width, lanes_eff, dev["order"], n, None)
+            pass
+        if fits.any():
+            groups.append((lanes, np.flatnonzero(fits)))
+        if (~fits).any():
+            groups.append((0, np.flatnonzero(~fits)))
+    else:
+        groups.append((0, np.arange(n)))
+    keep = []
+    for ln, idx in groups:
+        # length-sorted processing order: query length (segment), then target length
+        idx = idx[np.lexsort((-tlen[idx], -qlen[idx]))]
+        mq, nq = int(qlen[idx].max()), int(qlen[idx].min())
+        keep.append(run(width, ln, idx, max_q=mq, min_q=nq))
+        plan = _lib.plan_query(max(1, mq), n_sym, width, ln)
+        res["lanes_used"][idx] = plan.lanes
+        res["seg_len"][idx] = np.maximum(1, (qlen[idx] + plan.lanes - 1) // plan.lanes)
     if width == 16:
         lst = torch.empty(n, dtype=torch.int32, device="cuda")
         cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         _lib.check(L.sw_collect_flagged(_ptr(out["flags"]), n, _lib.FLAG_RESCUE, _ptr(lst),
                                         _ptr(cnt), st))
-        l32 = lanes_eff if lanes_eff and lanes_eff <= 32 else 0
-        try:
-            _lib.plan_query(max_q, n_sym, 32, l32)
-        except _lib.SwError:
-            l32 = 0
-        run(32, l32, lst, 0, cnt)
-    return {k: v.cpu().numpy() for k, v in out.items()}
+        mq = int(qlen.max())
+        _lib.check(L.sw_pairs_align(32, 0, kid, _ptr(dev["qry"]), _ptr(dev["qs"]),
+                                    _ptr(dev["ql"]), _ptr(dev["tgt"]), _ptr(dev["ts"]),
+                                    _ptr(dev["tl"]), _ptr(lst), 0, _ptr(cnt), 0, mq,
+                                    _ptr(sub_t), n_sym, go, ge, bias, max_sub,
+                                    *[_ptr(x) for x in pp], _ptr(out["score"]),
+                                    _ptr(out["ref_end"]), _ptr(out["query_end"]),
+                                    _ptr(out["flags"]), None, _ptr(pstats), st))
+    for k, v in out.items():
+        res[k] = v.cpu().numpy()
+    res["score"] = res["score"].astype(np.int64)
+    if stats:
+        res["pass_stats"] = pstats.cpu().numpy()
+    return res
 
 
 def batch_align(kernel_id, p, flat_q, q_off, flat_r, r_off, match_a, mis_a, go_a, ge_a):
-    """src/_compiled.py:504-529: per-pair 4x4 DNA schemes; returns
-    ``(scores int64, overflow uint8, ref_end, query_end)``."""
+    """src/_compiled.py:504-529: per-pair 4x4 DNA schemes, kernel_id 0 = lazy-F with
+    early exit, 1 = lazy-F full, 2 = scan. Returns ``(scores int64[n], overflow
+    uint8[n], counters int64[n, 7])`` like the reference. Lazy-F runs in
+    reference-mirroring mode so, for pairs whose reference layout fits
+    (ceil(m/p) <= 32), the counters equal the reference's exactly."""
+    kernel = {0: "lazyf-mirror", 1: "lazyf-noexit-mirror", 2: "scan"}[int(kernel_id)]
+    ref_kernel = {0: "lazyf", 1: "lazyf-noexit", 2: "scan"}[int(kernel_id)]
+    r = pairs_align(flat_q, q_off, flat_r, r_off, kernel=kernel, lanes=int(p), match_a=match_a,
+                    mis_a=mis_a, go_a=go_a, ge_a=ge_a, stats=True)
+    n = r["score"].shape[0]
+    tl = np.diff(np.asarray(r_off, dtype=np.int64))
+    counters = np.zeros((n, 7), dtype=np.int64)
+    for t in range(n):
+        counters[t] = counters_from_stats(ref_kernel, int(tl[t]), int(r["seg_len"][t]),
+                                          int(r["lanes_used"][t]), int(r["pass_stats"][t, 0]),
+                                          int(r["pass_stats"][t, 1]))
+    return (r["score"], (r["flags"] & _lib.FLAG_REF_OVERFLOW).astype(np.uint8), counters)
+
+
+def batch_align_coords(kernel_id, p, flat_q, q_off, flat_r, r_off, match_a, mis_a, go_a, ge_a):
+    """batch_align plus end coordinates: ``(scores, overflow, ref_end, query_end)``."""
     kernel = {0: "lazyf", 1: "lazyf-noexit", 2: "scan"}[int(kernel_id)]
     r = pairs_align(flat_q, q_off, flat_r, r_off, kernel=kernel, lanes=int(p), match_a=match_a,
                     mis_a=mis_a, go_a=go_a, ge_a=ge_a)
-    return (r["score"].astype(np.int64), (r["flags"] & _lib.FLAG_REF_OVERFLOW).astype(np.uint8),
-            r["ref_end"], r["query_end"])
+    return (r["score"], (r["flags"] & _lib.FLAG_REF_OVERFLOW).astype(np.uint8), r["ref_end"],
+            r["query_end"])
 
 
 def batch_oracle_scores(flat_q, q_off, flat_r, r_off, match_a, mis_a, go_a, ge_a):

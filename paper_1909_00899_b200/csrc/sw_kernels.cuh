@@ -176,6 +176,7 @@ struct SwArgs {
   int32_t* query_end;
   uint8_t* flags;
   int32_t* col_passes;       // optional: per-column correction passes (job 0 only)
+  int64_t* pass_stats;       // optional [n_jobs][2]: total lazy-F passes, early-exit columns
   const int64_t* n_jobs_dev; // optional device-side job count (overrides n_jobs; rescue launches)
   int32_t pair_stride;       // pairs mode: words per group profile slice ((A+1)*Lmax*T)
 };
@@ -344,6 +345,7 @@ sw_striped_kernel(const SwArgs a) {
 #pragma unroll
     for (int c = 0; c < LMAX; ++c) { H[c] = 0u; E[c] = 0u; }
     uint32_t carry = 0u;
+    int64_t tot_passes = 0, breaks = 0;  // lazy-F statistics (reference op counters)
     int gb = 0;                       // best of all earlier columns, group-wide
     int bv = 0, bcol = -1, bq = -1;   // this thread's first-maximum record
     const int nullsym = A;
@@ -496,6 +498,10 @@ sw_striped_kernel(const SwArgs a) {
         }
         if (a.col_passes != nullptr && job == 0 && valid && t == 0 && i < len)
           a.col_passes[i] = passes;
+        if (i < len) {
+          tot_passes += passes;
+          breaks += (a.early_exit && passes < P) ? 1 : 0;
+        }
       }
     }
 
@@ -519,6 +525,10 @@ sw_striped_kernel(const SwArgs a) {
       if (a.n_jobs_dev) fl |= FLAG_RESCUED;  // device-counted launches are rescue passes
       if (best == 0) { col = -1; q = -1; }
       a.score[job] = best;
+      if (a.pass_stats) {
+        a.pass_stats[2 * job] = tot_passes;
+        a.pass_stats[2 * job + 1] = breaks;
+      }
       if (a.ref_end) a.ref_end[job] = col;
       if (a.query_end) a.query_end[job] = q;
       if (a.flags) a.flags[job] = fl;

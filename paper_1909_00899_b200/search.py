@@ -162,7 +162,7 @@ class DatabaseSearch:
                                  sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
                                  _ptr(d.length), None, n, None, _ptr(o["score"]),
                                  _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
-                                 None, st))
+                                 None, None, st))
         lst, cnt = o["_rescue"]
         _lib.check(L.sw_collect_flagged(_ptr(o["flags"]), n, _lib.FLAG_RESCUE, _ptr(lst),
                                         _ptr(cnt), st))
@@ -170,7 +170,7 @@ class DatabaseSearch:
                                  sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
                                  _ptr(d.length), _ptr(lst), 0, _ptr(cnt), _ptr(o["score"]),
                                  _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
-                                 None, st))
+                                 None, None, st))
         self.launches += 3
         return o
 
@@ -211,7 +211,7 @@ class DatabaseSearch:
                                      sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes),
                                      ptr(d.start, a), ptr(d.length, a), None, b - a, None,
                                      ptr(o["score"], a), ptr(o["ref_end"], a),
-                                     ptr(o["query_end"], a), ptr(o["flags"], a), None, st))
+                                     ptr(o["query_end"], a), ptr(o["flags"], a), None, None, st))
             self.launches += 1
         lst, cnt = o["_rescue"]
         _lib.check(L.sw_collect_flagged(_ptr(o["flags"]), n, _lib.FLAG_RESCUE, _ptr(lst),
@@ -220,7 +220,7 @@ class DatabaseSearch:
                                  sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
                                  _ptr(d.length), _ptr(lst), 0, _ptr(cnt), _ptr(o["score"]),
                                  _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
-                                 None, st))
+                                 None, None, st))
         self.launches += 2
         return o
 

@@ -87,12 +87,59 @@ def acceptance_sweep_inputs(n=10_000):
     return flat_q, q_off, flat_t, t_off, match, mismatch, gap_open, gap_extend
 
 
+RUNNER_FASTA_Q = ">q1 first\nACGTACGTTGCA\n>q2\nGGGCCCAAATTTACGT\nacgtnn\n"
+RUNNER_FASTA_T = ">t1\nTTGCAACGTACG\n\n>t2 second target\nACGTNACGTTTTGGGCCA\n"
+RUNNER_MATRIX = "A C G T N\n 5 -4 -4 -4 -2\n-4  5 -4 -4 -2\n-4 -4  5 -4 -2\n-4 -4 -4  5 -2\n-2 -2 -2 -2 -1\n"
+
+
+def runner_fixtures() -> None:
+    """The reference runner's TSV (src/runner.py:162-191) for seeded random pairs with
+    every kernel, and for FASTA files + a matrix file; time_ns is masked later."""
+    import io
+    import tempfile
+
+    from swscan.runner import RunConfig, run
+
+    out = {}
+    for kern in ("scalar", "lazyf", "lazyf-noexit", "scan"):
+        for lanes in (8, 16):
+            buf = io.StringIO()
+            rc = run(RunConfig(kernel=kern, lanes=lanes, random_count=150, seed=11, len_max=200,
+                               match=3, mismatch=-2, gap_open=4, gap_extend=1), out=buf)
+            assert rc == 0
+            out[f"random_{kern}_l{lanes}"] = buf.getvalue()
+    with tempfile.TemporaryDirectory() as d:
+        paths = {}
+        for name, text in (("q.fa", RUNNER_FASTA_Q), ("t.fa", RUNNER_FASTA_T),
+                           ("m.txt", RUNNER_MATRIX)):
+            paths[name] = os.path.join(d, name)
+            with open(paths[name], "w") as fh:
+                fh.write(text)
+        for kern in ("scan", "lazyf"):
+            for mode in ("all-vs-all", "zip"):
+                buf = io.StringIO()
+                rc = run(RunConfig(kernel=kern, lanes=4, matrix_path=paths["m.txt"],
+                                   query_path=paths["q.fa"], target_path=paths["t.fa"],
+                                   pairs_mode=mode, gap_open=6, gap_extend=2), out=buf)
+                assert rc == 0
+                out[f"fasta_{kern}_{mode}"] = buf.getvalue()
+    out["inputs"] = {"query_fasta": RUNNER_FASTA_Q, "target_fasta": RUNNER_FASTA_T,
+                     "matrix": RUNNER_MATRIX}
+    with open(os.path.join(HERE, "runner_tsv.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--full-config5", action="store_true",
                     help="also score the full 65,536 x 1,048,576 config 5 (minutes)")
+    ap.add_argument("--only-runner", action="store_true",
+                    help="only regenerate the runner TSV fixtures")
     args = ap.parse_args()
     swscan, C = _import_reference()
+    runner_fixtures()
+    if args.only_runner:
+        return
     from swscan.kernels import weighted_max_scan
     from swscan.oracle import correct_lazyf_full, scan_sequential, sw_scalar
     from swscan.profile import build_profile

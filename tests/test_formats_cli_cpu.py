@@ -1,0 +1,91 @@
+"""Formats, runner validation and CLI usage errors (no device work)."""
+
+from __future__ import annotations
+
+import io
+
+import numpy as np
+import pytest
+
+from paper_1909_00899_b200 import cli, formats, runner
+from paper_1909_00899_b200.scoring import Alphabet, ScoringScheme
+
+
+def test_parse_fasta_records_case_blank_crlf():
+    recs = formats.parse_fasta(b">a desc here\r\nacgt\r\n\r\nTT\n>b\nG\n")
+    assert [(r.id, r.description, r.sequence) for r in recs] == [
+        ("a", "desc here", "ACGTTT"), ("b", "", "G")]
+    assert formats.parse_fasta(io.StringIO(">x\nAC\n"))[0].sequence == "AC"
+
+
+@pytest.mark.parametrize("bad", [b"ACGT\n>a\nA\n", b">a\n\n>b\nA\n", b">\nACGT\n",
+                                 b">a\nAC\xff\n"])
+def test_parse_fasta_errors(bad):
+    with pytest.raises(formats.MalformedFasta):
+        formats.parse_fasta(bad)
+
+
+def test_parse_fasta_alphabet_check():
+    with pytest.raises(formats.MalformedFasta):
+        formats.parse_fasta(b">a\nACGX\n", Alphabet.dna())
+    assert formats.parse_fasta(b">a\nacgn\n", Alphabet.dna())[0].sequence == "ACGN"
+
+
+def test_parse_matrix_and_errors():
+    alph, rows = formats.parse_matrix("A B\n1 -1\n-1 2\n")
+    assert alph.symbols == "AB" and rows == ((1, -1), (-1, 2))
+    for bad in ("", "AB C\n1 2\n3 4\n", "A A\n1 1\n1 1\n", "A B\n1 2\n", "A B\n1 2\n3\n",
+                "A B\n1 x\n3 4\n"):
+        with pytest.raises(formats.MalformedMatrix):
+            formats.parse_matrix(bad)
+
+
+def test_encode_records_and_packed_db():
+    recs = formats.parse_fasta(">a\nACGT\n>b\nGG\n>c\nTTTAC\n")
+    codes, off = formats.encode_records(recs, Alphabet("ACGT"))
+    assert codes.tolist() == [0, 1, 2, 3, 2, 2, 3, 3, 3, 0, 1] and off.tolist() == [0, 4, 6, 11]
+    _, packed = formats.load_fasta_db(">a\nACGT\n>b\nGG\n>c\nTTTAC\n", Alphabet("ACGT"),
+                                      pin=False)
+    assert packed.ids.tolist() == [2, 0, 1]  # length-descending physical order
+    assert packed.length.tolist() == [5, 4, 2]
+    assert packed.codes[:5].tolist() == [3, 3, 3, 0, 1]
+
+
+def test_generate_pairs_is_the_reference_generator():
+    # draw order (query len, target len, query, target) and wildcard exclusion
+    a = runner.generate_pairs(5, 3, 9, 42, Alphabet.dna())
+    rng = np.random.default_rng(42)
+    for q, t in a:
+        lq = int(rng.integers(3, 10))
+        lt = int(rng.integers(3, 10))
+        assert q == "".join("ACGT"[i] for i in rng.integers(0, 4, lq))
+        assert t == "".join("ACGT"[i] for i in rng.integers(0, 4, lt))
+    assert runner.generate_pairs(5, 3, 9, 42, Alphabet.dna()) == a
+    with pytest.raises(ValueError):
+        runner.generate_pairs(-1, 1, 2, 0, Alphabet.dna())
+
+
+def test_runner_validation_returns_1(capsys):
+    assert runner.run(runner.RunConfig(kernel="bogus", random_count=1)) == 1
+    assert runner.run(runner.RunConfig(lanes=3, random_count=1)) == 1
+    assert runner.run(runner.RunConfig(query_path="/nonexistent.fa",
+                                       target_path="/nonexistent.fa")) == 1
+    assert "error:" in capsys.readouterr().err
+
+
+@pytest.mark.parametrize("argv", [["--random", "3", "--query", "q.fa"], [], ["--random", "-1"],
+                                  ["--random", "2", "--bench", "0"],
+                                  ["--random", "2", "--len-min", "5", "--len-max", "2"],
+                                  ["--random", "2", "--lanes", "3"]])
+def test_cli_usage_errors_exit_2(argv):
+    with pytest.raises(SystemExit) as e:
+        cli.main(argv)
+    assert e.value.code == 2
+
+
+def test_scheme_from_matrix_file(tmp_path):
+    f = tmp_path / "m.txt"
+    f.write_text("A C\n2 -3\n-3 2\n")
+    alph, sch = runner._build_scheme(runner.RunConfig(matrix_path=str(f), gap_open=5,
+                                                      gap_extend=2))
+    assert alph.symbols == "AC" and sch == ScoringScheme(((2, -3), (-3, 2)), 5, 2)

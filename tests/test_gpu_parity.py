@@ -96,9 +96,18 @@ def test_acceptance_sweep(A, oracle, kernel_id, p):
     g = golden("acceptance_sweep.npz")
     fq, qo, ft, to, match, mis, go_a, ge_a = acceptance_sweep_inputs()
     kern = ("lazyf", "lazyf-noexit", "scan")[kernel_id]
-    sc, ov, re_, qe = A.batch_align(kernel_id, p, fq, qo, ft, to, match, mis, go_a, ge_a)
+    sc, ov, re_, qe = A.batch_align_coords(kernel_id, p, fq, qo, ft, to, match, mis, go_a, ge_a)
     assert (sc == g["oracle"]).all()
     assert (ov == g[f"overflow_{kern}_p{p}"]).all()
+    # the reference's (scores, overflow, counters) triple; counters exact where the
+    # reference layout fits the registers (ceil(m/p) <= 32)
+    sc2, ov2, cnt = A.batch_align(kernel_id, p, fq, qo, ft, to, match, mis, go_a, ge_a)
+    assert (sc2 == g["oracle"]).all() and (ov2 == ov).all()
+    want = g[f"counters_{kern}_p{p}"]
+    qlen = np.diff(qo)[: want.shape[0]]
+    fits = (qlen + p - 1) // p <= 32
+    assert fits.sum() > 0
+    assert (cnt[: want.shape[0]][fits] == want[fits]).all()
     _, rend, qend = oracle.batch_scalar(fq, qo, ft, to, match_a=match, mis_a=mis, go_a=go_a,
                                         ge_a=ge_a)
     assert (re_ == rend).all() and (qe == qend).all()
@@ -371,7 +380,7 @@ def test_config2_full_database_properties(A, oracle):
                                        prof.bias, prof.max_sub, _ptr(tgt), _ptr(start),
                                        _ptr(length), None, n, None, _ptr(o32["score"]),
                                        _ptr(o32["ref_end"]), _ptr(o32["query_end"]), _ptr(fl),
-                                       None, _stream()))
+                                       None, None, _stream()))
     for k in ("score", "ref_end", "query_end"):
         assert (o32[k].cpu().numpy() == res["scan"][k]).all(), k
     rng = np.random.default_rng(0xD0B)
@@ -404,3 +413,49 @@ def test_config3_large_batch_properties(A, oracle):
     sc, re_, qe = oracle.batch_scalar(fq, qo, fr, ro, sub=w.scheme.as_array(), go=6, ge=1)
     assert (r1["score"][pick] == sc).all()
     assert (r1["ref_end"][pick] == re_).all() and (r1["query_end"][pick] == qe).all()
+
+
+# ---- runner / TSV ----------------------------------------------------------
+
+
+def _mask_time(tsv: str) -> list[list[str]]:
+    rows = []
+    for line in tsv.strip().splitlines():
+        cols = line.split("\t")
+        if len(cols) >= 7 and cols[0] != "query_id":
+            cols[6] = "*"
+        rows.append(cols)
+    return rows
+
+
+def test_runner_tsv_matches_reference(A, tmp_path):
+    import io
+
+    from paper_1909_00899_b200 import runner
+
+    g = golden("runner_tsv.json")
+    for kern in ("scalar", "lazyf", "lazyf-noexit", "scan"):
+        for lanes in (8, 16):
+            buf = io.StringIO()
+            rc = runner.run(runner.RunConfig(kernel=kern, lanes=lanes, random_count=150, seed=11,
+                                             len_max=200, match=3, mismatch=-2, gap_open=4,
+                                             gap_extend=1), out=buf)
+            assert rc == 0
+            assert _mask_time(buf.getvalue()) == _mask_time(g[f"random_{kern}_l{lanes}"]), (kern, lanes)
+    paths = {}
+    for name, key in (("q.fa", "query_fasta"), ("t.fa", "target_fasta"), ("m.txt", "matrix")):
+        paths[name] = tmp_path / name
+        paths[name].write_text(g["inputs"][key])
+    for kern in ("scan", "lazyf"):
+        for mode in ("all-vs-all", "zip"):
+            buf = io.StringIO()
+            rc = runner.run(runner.RunConfig(kernel=kern, lanes=4, matrix_path=str(paths["m.txt"]),
+                                             query_path=str(paths["q.fa"]),
+                                             target_path=str(paths["t.fa"]), pairs_mode=mode,
+                                             gap_open=6, gap_extend=2), out=buf)
+            assert rc == 0
+            assert _mask_time(buf.getvalue()) == _mask_time(g[f"fasta_{kern}_{mode}"]), (kern, mode)
+    # --coords appends end coordinates checked against the oracle elsewhere
+    buf = io.StringIO()
+    assert runner.run(runner.RunConfig(random_count=5, seed=3, coords=True), out=buf) == 0
+    assert buf.getvalue().splitlines()[0].endswith("ref_end\tquery_end")
