@@ -44,6 +44,8 @@ void init_tables() {
   swb_fill_exact_t8_g2_a(g_exact); swb_fill_exact_t8_g2_b(g_exact);
   swb_fill_exact_t16_g0_b(g_exact); swb_fill_exact_t16_g1_b(g_exact); swb_fill_exact_t16_g2_b(g_exact);
   swb_fill_exact_t32_g0_b(g_exact); swb_fill_exact_t32_g1_b(g_exact); swb_fill_exact_t32_g2_b(g_exact);
+  swb_fill_exact_t4_g0_b(g_exact); swb_fill_exact_t4_g1_b(g_exact); swb_fill_exact_t4_g2_b(g_exact);
+  swb_fill_exact_t4_g0_a(g_exact); swb_fill_exact_t4_g1_a(g_exact); swb_fill_exact_t4_g2_a(g_exact);
   swb_fill_chain(g_chain, g_chain_prof);
   swb_fill_w16_scan(g_tab[0][VAR_SCAN]);
   swb_fill_w16_lazyf(g_tab[0][VAR_LAZYF]);
@@ -94,9 +96,10 @@ int plan(int m, int n_sym, int width, int lanes, sw_plan_t* out) {
       return fail(SW_ENOTSUP, "lanes %d outside the warp kernels' range for width %d", lanes, width);
     P = lanes;
   } else {
-    // smallest P whose segment fits 32 register words, but at least 16 lanes for
-    // 16-bit (8 threads) so one warp holds 4 alignments in flight.
-    P = width == 16 ? 16 : 8;
+    // smallest P whose segment fits 32 register words (longer segments amortise the
+    // per-column scan): 8 stripes (4 threads, 8 alignments per warp) in 16-bit,
+    // measured +16 % over 16 stripes on config 3 (150-residue reads).
+    P = 8;
     while ((m + P - 1) / P > 32 && P < 32 * lpw) P *= 2;
   }
   const int T = P / lpw;

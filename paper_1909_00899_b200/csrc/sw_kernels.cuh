@@ -632,6 +632,7 @@ using ExactTable = const void* [kNumGe][kNumT][33];
 #define SWB_X_DECL(T, GE, PART) void swb_fill_exact_t##T##_g##GE##_##PART(swb::ExactTable& t);
 SWB_X_DECL(8, 0, a) SWB_X_DECL(8, 0, b) SWB_X_DECL(8, 1, a) SWB_X_DECL(8, 1, b)
 SWB_X_DECL(8, 2, a) SWB_X_DECL(8, 2, b) SWB_X_DECL(16, 0, b) SWB_X_DECL(16, 1, b)
-SWB_X_DECL(16, 2, b) SWB_X_DECL(32, 0, b) SWB_X_DECL(32, 1, b) SWB_X_DECL(32, 2, b)
+SWB_X_DECL(16, 2, b) SWB_X_DECL(32, 0, b) SWB_X_DECL(32, 1, b) SWB_X_DECL(32, 2, b) SWB_X_DECL(4, 0, b) SWB_X_DECL(4, 1, b) SWB_X_DECL(4, 2, b)
+SWB_X_DECL(4, 0, a) SWB_X_DECL(4, 1, a) SWB_X_DECL(4, 2, a)
 #undef SWB_X_DECL
 void swb_fill_chain(const void* (&tab)[2][4], const void* (&ptab)[2]);

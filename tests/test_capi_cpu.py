@@ -51,6 +51,8 @@ def test_plan_reproduces_reference_layout():
             assert pl.lmax >= L and pl.prof_words == 5 * L * (p // 2)
     auto = _lib.plan_query(464, 20, 16, 0)
     assert (auto.lanes, auto.seg_len) == (16, 29)
+    auto = _lib.plan_query(150, 4, 16, 0)
+    assert (auto.lanes, auto.threads, auto.seg_len) == (8, 4, 19)
     with pytest.raises(_lib.SwError):
         _lib.plan_query(10, 4, 24, 0)
     with pytest.raises(_lib.SwError):

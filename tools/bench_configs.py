@@ -90,7 +90,7 @@ def long_pair(name, w, reps, width=32):
          path="strip pipeline (sw_align_long)")
 
 
-def pairs(name, w, reps, kernels=("scan", "lazyf")):
+def pairs(name, w, reps, kernels=("scan", "lazyf"), lanes=0):
     L = _lib.load()
     n = w.n_pairs
     qlen = np.diff(w.q_off).astype(np.int32)
@@ -106,7 +106,7 @@ def pairs(name, w, reps, kernels=("scan", "lazyf")):
         kid = _lib.KERNEL_IDS[kern]
 
         def run():
-            _lib.check(L.sw_pairs_align(16, 0, kid, _ptr(dev["q"]), _ptr(dev["qs"]), _ptr(dev["ql"]),
+            _lib.check(L.sw_pairs_align(16, lanes, kid, _ptr(dev["q"]), _ptr(dev["qs"]), _ptr(dev["ql"]),
                                         _ptr(dev["t"]), _ptr(dev["ts"]), _ptr(dev["tl"]), None, n,
                                         None, int(qlen.min()), int(qlen.max()), _ptr(sub),
                                         sch.n_symbols, sch.gap_open, sch.gap_extend, sch.bias,
@@ -114,7 +114,7 @@ def pairs(name, w, reps, kernels=("scan", "lazyf")):
                                         _ptr(out["r"]), _ptr(out["q"]), _ptr(fl), None, None, _stream()))
 
         ms = timed(run, reps)
-        emit(config=name, kernel=kern, width=16, pairs=n, ms=round(ms, 3),
+        emit(config=name, kernel=kern, width=16, pairs=n, lanes=lanes, ms=round(ms, 3),
              gcups=round(w.cells / ms / 1e6, 3), path="pairs kernel (per-pair profiles)")
 
 
@@ -123,6 +123,7 @@ def main() -> None:
     ap.add_argument("--configs", default="1,3,4,5")
     ap.add_argument("--c3-pairs", type=int, default=1 << 20)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--c3-lanes", default="0")
     args = ap.parse_args()
     cfgs = {int(x) for x in args.configs.split(",")}
     if 1 in cfgs:
@@ -130,7 +131,10 @@ def main() -> None:
         single_pair("config1", w, ("scan", "lazyf", "lazyf-noexit"), 0, args.reps * 10)
         single_pair("config1", w, ("scan", "lazyf"), 64, args.reps * 10)
     if 3 in cfgs:
-        pairs(f"config3[{args.c3_pairs} pairs]", W.config3(n_pairs=args.c3_pairs), args.reps)
+        w3 = W.config3(n_pairs=args.c3_pairs)
+        for ln in (int(x) for x in args.c3_lanes.split(",")):
+            pairs(f"config3[{args.c3_pairs} pairs]", w3, args.reps, lanes=ln,
+                  kernels=("scan", "lazyf") if ln == 0 else ("scan",))
     if 4 in cfgs:
         w = W.config4()
         single_pair("config4", w, ("scan", "lazyf", "lazyf-noexit"), 0, args.reps)
