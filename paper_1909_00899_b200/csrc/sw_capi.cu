@@ -46,6 +46,10 @@ void init_tables() {
   swb_fill_exact_t32_g0_b(g_exact); swb_fill_exact_t32_g1_b(g_exact); swb_fill_exact_t32_g2_b(g_exact);
   swb_fill_exact_t4_g0_b(g_exact); swb_fill_exact_t4_g1_b(g_exact); swb_fill_exact_t4_g2_b(g_exact);
   swb_fill_exact_t4_g0_a(g_exact); swb_fill_exact_t4_g1_a(g_exact); swb_fill_exact_t4_g2_a(g_exact);
+  swb_fill_exact_t4_g0_c(g_exact); swb_fill_exact_t4_g1_c(g_exact); swb_fill_exact_t4_g2_c(g_exact);
+  swb_fill_exact_t4_g0_d(g_exact); swb_fill_exact_t4_g1_d(g_exact); swb_fill_exact_t4_g2_d(g_exact);
+  swb_fill_exact_t4_g0_e(g_exact); swb_fill_exact_t4_g1_e(g_exact); swb_fill_exact_t4_g2_e(g_exact);
+  swb_fill_exact_t4_g0_f(g_exact); swb_fill_exact_t4_g1_f(g_exact); swb_fill_exact_t4_g2_f(g_exact);
   swb_fill_chain(g_chain, g_chain_prof);
   swb_fill_w16_scan(g_tab[0][VAR_SCAN]);
   swb_fill_w16_lazyf(g_tab[0][VAR_LAZYF]);
@@ -99,21 +103,34 @@ int plan(int m, int n_sym, int width, int lanes, sw_plan_t* out) {
     // smallest P whose segment fits 32 register words (longer segments amortise the
     // per-column scan): 8 stripes (4 threads, 8 alignments per warp) in 16-bit,
     // measured +16 % over 16 stripes on config 3 (150-residue reads).
-    P = 8;
-    while ((m + P - 1) / P > 32 && P < 32 * lpw) P *= 2;
+    // Segments beyond the runtime-L kernels' 32 words exist only as exact 16-bit
+    // scan instances (register-resident, 2 CTAs/SM); the auto layout takes them
+    // when they exist (SWB_PLAN_MAX_L caps the segment length for experiments).
+    std::call_once(g_once, init_tables);
+    int cap = kExactLmax;
+    if (const char* e = getenv("SWB_PLAN_MAX_L")) cap = atoi(e);
+    P = 32 * lpw;
+    for (int PP = 8; PP <= 32 * lpw; PP *= 2) {
+      const int LL = (m + PP - 1) / PP;
+      if (LL <= kLmaxSet[kNumLmax - 1] && LL <= cap) { P = PP; break; }
+      if (width == 16 && LL <= cap && LL <= kExactLmax && g_exact[0][ilog2(PP / lpw)][LL]) {
+        P = PP;
+        break;
+      }
+    }
   }
   const int T = P / lpw;
   int L = (m + P - 1) / P;
   if (L < 1) L = 1;
-  const int li = lmax_index(L);
-  if (li < 0)
+  int li = lmax_index(L);
+  if (li < 0 && !(L <= kExactLmax && width == 16 && g_exact[0][ilog2(T)][L]))
     return fail(SW_ENOTSUP, "query length %d needs %d words per lane at %d lanes (max %d)", m, L, P,
                 kLmaxSet[kNumLmax - 1]);
   out->width = width;
   out->lanes = P;
   out->threads = T;
   out->seg_len = L;
-  out->lmax = kLmaxSet[li];
+  out->lmax = li >= 0 ? kLmaxSet[li] : L;  // lmax > 32: exact-instance-only plan
   out->m = m;
   out->n_sym = n_sym;
   out->prof_words = (n_sym + 1) * L * T;
@@ -268,7 +285,9 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
   if (!decode_kernel(kernel, &var, &early)) return fail(SW_EINVAL, "unknown kernel %d", kernel);
   const int wi = p->width == 16 ? 0 : 1;
   const int li = lmax_index(p->lmax);
-  if (li < 0 || kLmaxSet[li] != p->lmax) return fail(SW_EINVAL, "bad plan lmax %d", p->lmax);
+  if (li >= 0 && kLmaxSet[li] != p->lmax) return fail(SW_EINVAL, "bad plan lmax %d", p->lmax);
+  if (li < 0 && !(wi == 0 && var == VAR_SCAN))
+    return fail(SW_ENOTSUP, "segment length %d only has exact 16-bit scan kernels", p->seg_len);
   const void* fn = nullptr;
   int block = 256;
   if (wi == 0 && var == VAR_SCAN) {
@@ -276,7 +295,7 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
     fn = g_exact[gi][ilog2(p->threads)][p->seg_len];
     if (fn) block = 128;
   }
-  if (!fn) fn = g_tab[wi][var][ilog2(p->threads)][li];
+  if (!fn && li >= 0) fn = g_tab[wi][var][ilog2(p->threads)][li];
   if (!fn) return fail(SW_ENOTSUP, "no kernel for width %d, threads %d", p->width, p->threads);
   SwArgs a;
   std::memset(&a, 0, sizeof a);
@@ -346,7 +365,7 @@ int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8
     fn = g_exact[gi][ilog2(p.threads)][p.seg_len];
     if (fn) max_block = 128;
   }
-  if (!fn) fn = g_tab[wi][var][ilog2(p.threads)][lmax_index(p.lmax)];
+  if (!fn && lmax_index(p.lmax) >= 0) fn = g_tab[wi][var][ilog2(p.threads)][lmax_index(p.lmax)];
   if (!fn) return fail(SW_ENOTSUP, "no kernel for width %d, threads %d", width, p.threads);
   SwArgs a;
   std::memset(&a, 0, sizeof a);

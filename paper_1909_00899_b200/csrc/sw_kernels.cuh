@@ -197,13 +197,13 @@ struct SwArgs {
 #define SWB_UNROLL(n) SWB_PRAGMA(unroll n)
 
 template <class Wd, int T, int LMAX, int VAR, bool EXACT = false, int GE = 0>
-__global__ void __launch_bounds__(EXACT ? 128 : 256, EXACT ? SWB_EXACT_MINB : 1)
+__global__ void __launch_bounds__(EXACT ? 128 : 256, EXACT ? (LMAX > 32 ? 2 : SWB_EXACT_MINB) : 1)
 sw_striped_kernel(const SwArgs a) {
   // GE > 0: gap-extend penalty known at compile time, so every decay constant
   // (j*ge, k*L*ge) is an immediate operand of VIADDMNMX instead of a register.
   // EXACT: LMAX is the segment length itself (uniform-L launches); the word
   // loop is straight-line code the scheduler can software-pipeline.
-  static_assert(LMAX >= 1 && LMAX <= 32, "LMAX");
+  static_assert(LMAX >= 1 && (LMAX <= 32 || (EXACT && LMAX <= 64)), "LMAX");
   static_assert(T >= 1 && T <= 32 && (T & (T - 1)) == 0, "T");
   static_assert(Wd::LPW == 2 || T >= 2, "32-bit lanes need T >= 2");
   constexpr int P = Geo<Wd, T>::P;
@@ -627,12 +627,17 @@ void swb_fill_w32_mirror(swb::KernelTable& t);
 // exact-L instances (uniform segment length): [ge specialisation 0=runtime,1,2][log2 T][L]
 namespace swb {
 constexpr int kNumGe = 3;
-using ExactTable = const void* [kNumGe][kNumT][33];
+constexpr int kExactLmax = 64;
+using ExactTable = const void* [kNumGe][kNumT][kExactLmax + 1];
 }
 #define SWB_X_DECL(T, GE, PART) void swb_fill_exact_t##T##_g##GE##_##PART(swb::ExactTable& t);
 SWB_X_DECL(8, 0, a) SWB_X_DECL(8, 0, b) SWB_X_DECL(8, 1, a) SWB_X_DECL(8, 1, b)
 SWB_X_DECL(8, 2, a) SWB_X_DECL(8, 2, b) SWB_X_DECL(16, 0, b) SWB_X_DECL(16, 1, b)
 SWB_X_DECL(16, 2, b) SWB_X_DECL(32, 0, b) SWB_X_DECL(32, 1, b) SWB_X_DECL(32, 2, b) SWB_X_DECL(4, 0, b) SWB_X_DECL(4, 1, b) SWB_X_DECL(4, 2, b)
 SWB_X_DECL(4, 0, a) SWB_X_DECL(4, 1, a) SWB_X_DECL(4, 2, a)
+SWB_X_DECL(4, 0, c) SWB_X_DECL(4, 1, c) SWB_X_DECL(4, 2, c)
+SWB_X_DECL(4, 0, d) SWB_X_DECL(4, 1, d) SWB_X_DECL(4, 2, d)
+SWB_X_DECL(4, 0, e) SWB_X_DECL(4, 1, e) SWB_X_DECL(4, 2, e)
+SWB_X_DECL(4, 0, f) SWB_X_DECL(4, 1, f) SWB_X_DECL(4, 2, f)
 #undef SWB_X_DECL
 void swb_fill_chain(const void* (&tab)[2][4], const void* (&ptab)[2]);

@@ -49,8 +49,8 @@ def test_plan_reproduces_reference_layout():
             pl = _lib.plan_query(m, 4, 16, p)
             assert (pl.lanes, pl.threads, pl.seg_len) == (p, p // 2, L)
             assert pl.lmax >= L and pl.prof_words == 5 * L * (p // 2)
-    auto = _lib.plan_query(464, 20, 16, 0)
-    assert (auto.lanes, auto.seg_len) == (16, 29)
+    auto = _lib.plan_query(464, 20, 16, 0)  # exact long-segment instance: 8 stripes x 58 words
+    assert (auto.lanes, auto.threads, auto.seg_len, auto.lmax) == (8, 4, 58, 58)
     auto = _lib.plan_query(150, 4, 16, 0)
     assert (auto.lanes, auto.threads, auto.seg_len) == (8, 4, 19)
     with pytest.raises(_lib.SwError):
