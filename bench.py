@@ -259,7 +259,7 @@ def main() -> None:
     ek0, ek1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ek0.record(stream)
     for _ in range(k_reps):
-        _lib.check(L.sw_db_align(C.byref(p.plan16), _ptr(p.prof16), eng.kid, w.scheme.gap_open,
+        _lib.check(L.sw_db_align(C.byref(eng.plan16), _ptr(eng.prof16), eng.kid, w.scheme.gap_open,
                                  w.scheme.gap_extend, p.bias, p.max_sub, _ptr(d.codes),
                                  _ptr(d.start), _ptr(d.length), None, d.n, None,
                                  _ptr(o["score"]), _ptr(o["ref_end"]), _ptr(o["query_end"]),
@@ -335,16 +335,16 @@ def main() -> None:
                        "matrix": "synthetic-stand-in (BLOSUM62 not in container)",
                        "gaps": "open 11, extend 1 (reference convention)",
                        "l2": "inputs 359 MB > 126 MB L2 (no flush)",
-                       "parallelism": f"db-shard x{world}", "lanes": p.plan16.lanes,
-                       "seg_len": p.plan16.seg_len},
+                       "parallelism": f"db-shard x{world}", "lanes": eng.plan16.lanes,
+                       "seg_len": eng.plan16.seg_len},
             "roofline": {"bound": "dpx", "achieved": round(kernel_gcups, 2),
                          "peak": round(peak_gcups, 2), "unit": "GCUPS",
                          "frac": round(kernel_gcups / peak_gcups, 4),
                          # dram__bytes_read+write per launch of this kernel (one ncu --set
                          # full capture at this config, profiles/r01_config2_db_kernel.md)
                          "traffic": 516.44e6,
-                         "kernel": (f"sw_striped_kernel<W16,T={p.plan16.threads},"
-                                    f"L={p.plan16.seg_len},SCAN,exact,ge={w.scheme.gap_extend}>"),
+                         "kernel": (f"sw_striped_kernel<W16,T={eng.plan16.threads},"
+                                    f"L={eng.plan16.seg_len},{args.kernel.upper()},ge={w.scheme.gap_extend}>"),
                          "kernel_ms": round(k_ms, 3),
                          "peak_source": "live DPX probe (cell-update mix, 6 instr per 2 cells)",
                          "dpx_probe": {"mix_instr_per_s": dpx_instr_per_s,

@@ -158,6 +158,22 @@ class DeviceProfile:
     def lanes(self) -> int:
         return self.plan16.lanes
 
+    def for_kernel(self, kernel: str) -> tuple[_lib.Plan, torch.Tensor]:
+        """16-bit (plan, profile) usable by `kernel`: segments beyond 32 words exist
+        only for the scan kernel, so other kernels get a <= 32-word layout."""
+        if kernel == "scan" or self.plan16.lmax <= 32:
+            return self.plan16, self.prof16
+        if "short" not in self.extra:
+            P = 8
+            while (self.m + P - 1) // P > 32:
+                P *= 2
+            plan = _lib.plan_query(self.m, self.scheme.n_symbols, 16, P)
+            prof = torch.empty(plan.prof_words, dtype=torch.int32, device="cuda")
+            _lib.check(_lib.load().sw_profile_build(C.byref(plan), _ptr(self.query), _ptr(self.sub),
+                                                     self.bias, _ptr(prof), _stream()))
+            self.extra["short"] = (plan, prof)
+        return self.extra["short"]
+
     def ensure32(self) -> None:
         if self.plan32 is not None:
             return
@@ -257,7 +273,8 @@ def db_align(prof: DeviceProfile, tgt: torch.Tensor, start: torch.Tensor, length
     kid = _kernel_id(kernel)
     sch = prof.scheme
     st = _stream()
-    _lib.check(L.sw_db_align(C.byref(prof.plan16), _ptr(prof.prof16), kid, sch.gap_open,
+    plan16, prof16 = prof.for_kernel(kernel)
+    _lib.check(L.sw_db_align(C.byref(plan16), _ptr(prof16), kid, sch.gap_open,
                              sch.gap_extend, prof.bias, prof.max_sub, _ptr(tgt), _ptr(start),
                              _ptr(length), _ptr(order), n, None, _ptr(out["score"]),
                              _ptr(out["ref_end"]), _ptr(out["query_end"]), _ptr(out["flags"]),
@@ -350,7 +367,8 @@ def align_prebuilt(kernel: str, prof: DeviceProfile, bias=None, ref=None,
     if flags & _lib.FLAG_RESCUED:
         P, L_ = prof.plan32.lanes, prof.plan32.seg_len
     else:
-        P, L_ = prof.lanes, prof.seg_len
+        pl = prof.for_kernel(kernel)[0]
+        P, L_ = pl.lanes, pl.seg_len
     return _result_from(prof, kernel, n, L_, P, int(out["score"][0]), flags,
                         int(out["ref_end"][0]), int(out["query_end"][0]),
                         passes.cpu().numpy() if passes is not None else None)

@@ -141,6 +141,7 @@ class DatabaseSearch:
     def set_query(self, query) -> DeviceProfile:
         self.prof = build_profile_arrays(query, self.scheme, self.lanes)
         self.prof.ensure32()
+        self.plan16, self.prof16 = self.prof.for_kernel(self.kernel)
         self.launches += 2
         return self.prof
 
@@ -148,8 +149,8 @@ class DatabaseSearch:
         """Re-run the profile kernels for the current query (device-resident)."""
         L = _lib.load()
         p = self.prof
-        _lib.check(L.sw_profile_build(C.byref(p.plan16), _ptr(p.query), _ptr(p.sub), p.bias,
-                                      _ptr(p.prof16), _stream()))
+        _lib.check(L.sw_profile_build(C.byref(self.plan16), _ptr(p.query), _ptr(p.sub), p.bias,
+                                      _ptr(self.prof16), _stream()))
         self.launches += 1
 
     def align(self) -> dict:
@@ -158,7 +159,7 @@ class DatabaseSearch:
         p, d, o, sch = self.prof, self.dev, self.out, self.scheme
         st = _stream()
         n = d.n
-        _lib.check(L.sw_db_align(C.byref(p.plan16), _ptr(p.prof16), self.kid, sch.gap_open,
+        _lib.check(L.sw_db_align(C.byref(self.plan16), _ptr(self.prof16), self.kid, sch.gap_open,
                                  sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
                                  _ptr(d.length), None, n, None, _ptr(o["score"]),
                                  _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
@@ -207,7 +208,7 @@ class DatabaseSearch:
             if b <= a:
                 continue
             ptr = lambda t, i: C.c_void_p(t.data_ptr() + i * t.element_size())  # noqa: E731
-            _lib.check(L.sw_db_align(C.byref(p.plan16), _ptr(p.prof16), self.kid, sch.gap_open,
+            _lib.check(L.sw_db_align(C.byref(self.plan16), _ptr(self.prof16), self.kid, sch.gap_open,
                                      sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes),
                                      ptr(d.start, a), ptr(d.length, a), None, b - a, None,
                                      ptr(o["score"], a), ptr(o["ref_end"], a),
