@@ -355,6 +355,17 @@ int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8
   sw_plan_t p;
   int rc = plan(max_qlen, n_sym, width, lanes, &p);
   if (rc) return rc;
+  if (lmax_index(p.lmax) < 0) {
+    // long segments exist only as exact scan instances: other kernels and mixed
+    // segment lengths take the smallest stripe count with <= 32 words instead
+    const bool uniform = min_qlen > 0 && (min_qlen + p.lanes - 1) / p.lanes == p.seg_len;
+    if (var != VAR_SCAN || !uniform || per_pair) {
+      int P = 8;
+      while ((max_qlen + P - 1) / P > kLmaxSet[kNumLmax - 1]) P *= 2;
+      rc = plan(max_qlen, n_sym, width, P, &p);
+      if (rc) return rc;
+    }
+  }
   const int wi = width == 16 ? 0 : 1;
   const void* fn = nullptr;
   // every query of the batch has the same segment length: exact-L instance
