@@ -533,7 +533,7 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
     a.reverse = getenv("SWB_CHAIN_REVERSE") != nullptr;
   }
   const void* fn = g_chain[wi][g.li];
-  const size_t smem = (size_t)(n_sym + 1) * g.L * 32 * 4;
+  const size_t smem = (size_t)(n_sym + 1) * g.L * 32 * 4 + kChainK * (16 + 8);  // + tile staging
   if (smem > 48 * 1024) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(chain smem)");

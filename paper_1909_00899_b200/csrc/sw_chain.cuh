@@ -142,6 +142,9 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
     __syncwarp();
   }
   const uint32_t* prof_t = smem + t;
+  // per-tile staging: incoming (F_in, H_last, residue) per column, outgoing (F_out, H_last)
+  int4* tile_in = reinterpret_cast<int4*>(smem + (A + 1) * L * 32);
+  int2* tile_out = reinterpret_cast<int2*>(tile_in + kChainK);
   if (a.trace && t == 0) {  // diagnostics: SM of this strip, after the timeline
     unsigned smid;
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
@@ -208,15 +211,18 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
     if (tr31) tr31[3] = gtimer();
     __syncwarp();
     if (tr) tr[1] = gtimer();
-    int fo_l = 0, ho_l = 0;  // this tile's outgoing values (lane k holds column t0+k)
-    const int sym_l = t < kc ? (int)__ldg(a.ref + t0 + t) : 0;  // lane k: residue of column t0+k
+    // stage this tile's per-column inputs in shared memory: each column then reads
+    // them with one broadcast load instead of three shuffles
+    tile_in[t] = make_int4(fin_l, hl_l, t < kc ? (int)__ldg(a.ref + t0 + t) : 0, 0);
+    __syncwarp();
 
-    for (int k = 0; k < kc; ++k) {
-      const int64_t i = t0 + k;
-      const int sym = __shfl_sync(gmask, sym_l, k);
+    for (int col_k = 0; col_k < kc; ++col_k) {
+      const int64_t i = t0 + col_k;
+      const int4 tin = tile_in[col_k];
+      const int sym = tin.z;
       const uint32_t* pr = prof_t + sym * (L * 32);
-      const int fin = __shfl_sync(gmask, fin_l, k);
-      const int hlk = __shfl_sync(gmask, hl_l, k);
+      const int fin = tin.x;
+      const int hlk = tin.y;
       // diagonal for the strip's first cell: corrected H of strip b-1, column i-1
       uint32_t vh = Wd::template shift<T, 1>(wnext, t, gmask, sel[0]);
       if (t == 0) {  // lane 0 (low half of thread 0) takes the previous strip's value
@@ -228,7 +234,7 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
       constexpr int kCh = 8, kNch = (L + kCh - 1) / kCh;
       uint32_t cmk[kNch];
 #pragma unroll
-      for (int k = 0; k < kNch; ++k) cmk[k] = 0u;
+      for (int ch = 0; ch < kNch; ++ch) cmk[ch] = 0u;
 #pragma unroll
       for (int c = 0; c < L; ++c) {
         const uint32_t S = pr[c * 32];
@@ -273,8 +279,7 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
       }
       {
         int g = max(gb, cmx);
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) g = max(g, __shfl_xor_sync(gmask, g, off));
+        g = __reduce_max_sync(gmask, g);  // one REDUX for the strip-wide best
         gb = g;
       }
       // Alg. 6 scan inside the strip, then fold in the strip's incoming F
@@ -294,13 +299,12 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
       wnext = Wd::addmax(carry, NWRAP, H[L - 1]);       // corrected H of the last word
       const uint32_t fo = Wd::addmax(carry, NLD, F);    // true F leaving each lane
       // the strip's last lane (thread 31, top half) holds this column's boundary
-      // pair; park it in lane k so the tile leaves in one coalesced store
-      const int fo_k = __shfl_sync(gmask, Wd::get(fo, Wd::LPW - 1), T - 1);
-      const int ho_k = __shfl_sync(gmask, Wd::get(wnext, Wd::LPW - 1), T - 1);
-      if (t == k) { fo_l = fo_k; ho_l = ho_k; }
+      // pair; stage it so the tile leaves in one coalesced store
+      if (t == T - 1) tile_out[col_k] = make_int2(Wd::get(fo, Wd::LPW - 1), Wd::get(wnext, Wd::LPW - 1));
     }
+    __syncwarp();
     if (b + 1 < nb) {
-      if (t < kc) ring_out[(t0 + t) % RING] = make_int2(fo_l, ho_l);
+      if (t < kc) ring_out[(t0 + t) % RING] = tile_out[t];
       __syncwarp();
       if (t == 0) st_release(a.published + (size_t)b * 16, (unsigned long long)(t0 + kc));
     }
