@@ -32,7 +32,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 KernelTable g_tab[2][3];
 ExactTable g_exact;  // 16-bit scan, exact segment length
-const void* g_chain[2][4];  // strip pipeline [width][L = 4, 8, 16, 32]
+const void* g_chain[2][6];  // strip pipeline [width][L = 1, 2, 4, 8, 16, 32]
 const void* g_chain_prof[2];
 std::once_flag g_once;
 
@@ -430,14 +430,23 @@ struct ChainGeo {
 
 static ChainGeo chain_geo(int64_t m, int64_t n, int n_sym, int width) {
   const int lpw = width == 16 ? 2 : 1;
-  static const int Ls[4] = {4, 8, 16, 32};
+  static const int Ls[6] = {1, 2, 4, 8, 16, 32};
   ChainGeo g{};
   double best = 1e300;
-  for (int li = 0; li < 4; ++li) {
+  // measured per-column latency (cycles, 32-bit, B200) of one strip alone and of a
+  // strip in a full pipeline (~3.5 strips per SM); tools/chain_latency.py
+  static const double lat_alone[6] = {315, 322, 355, 402, 474, 670};
+  static const double lat_loaded[6] = {506, 485, 501, 533, 624, 822};
+  for (int li = 0; li < 6; ++li) {
     const int L = Ls[li];
     const int64_t rows = 32LL * lpw * L;
     const int64_t nb = (m + rows - 1) / rows;
-    const double cost = (double)(n + nb * kChainK) * (190.0 + 5.0 * L);
+    const double load = nb >= 518 ? 1.0 : (double)nb / 518.0;
+    const double lat = lat_alone[li] + load * (lat_loaded[li] - lat_alone[li]);
+    // every strip must be co-resident (cooperative launch): keep well inside
+    // 148 SMs x 16 one-warp CTAs unless no strip height fits
+    double cost = (double)(n + nb * kChainK) * lat;
+    if (nb > 148 * 16 && li < 5) cost *= 1e6;
     if (cost < best) {
       best = cost;
       g.li = li; g.L = L; g.nb = (int)(nb < 1 ? 1 : nb);
@@ -445,7 +454,7 @@ static ChainGeo chain_geo(int64_t m, int64_t n, int n_sym, int width) {
   }
   if (const char* force = getenv("SWB_CHAIN_L")) {  // debugging / tuning override
     const int L = atoi(force);
-    for (int li = 0; li < 4; ++li)
+    for (int li = 0; li < 6; ++li)
       if (Ls[li] == L) {
         const int64_t rows = 32LL * lpw * L;
         g.li = li; g.L = L; g.nb = (int)((m + rows - 1) / rows);

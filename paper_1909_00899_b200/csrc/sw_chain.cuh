@@ -154,6 +154,14 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
   uint32_t sel[6];
 #pragma unroll
   for (int s = 0; s < 6; ++s) sel[s] = Wd::shift_sel(t, 1 << s);
+  // scan-step selectors: lanes with no source keep their own value (harmless under
+  // max(relu(x - K*d), x)), which drops the zero-select from the 32-bit steps
+  uint32_t ssel[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) ssel[s] = Wd::scan_sel(t, 1 << s);
+  // first scan shift: lane 0 (thread 0, low half) receives the strip's incoming F,
+  // so the scan itself applies the lane * L * ge decay
+  const uint32_t sel_in = Wd::inject_sel(t);
   const int cl = Wd::CLAMP;
   const int go = a.go, ge = a.ge;
   const uint32_t NGO = Wd::splat(-min(go, cl));
@@ -167,9 +175,6 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
 #pragma unroll
   for (int s = 0; s < STEPS; ++s)
     NKD[s] = Wd::splat(-(int)min((int64_t)(1 << s) * L * (int64_t)ge, (int64_t)cl));
-  // decay of the incoming strip F to this thread's lanes: lane * L * ge
-  const uint32_t NLANE = Wd::pack(-(int)min((int64_t)t * L * ge, (int64_t)cl),
-                                  -(int)min((int64_t)(T + t) * L * ge, (int64_t)cl));
 
   uint32_t H[L], E[L];
 #pragma unroll
@@ -283,19 +288,19 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
         gb = g;
       }
       // Alg. 6 scan inside the strip, then fold in the strip's incoming F
-      uint32_t acc = Wd::template shift<T, 1>(F, t, gmask, sel[0]);
+      uint32_t acc = Wd::template shift_in<T>(F, Wd::splat(fin), t, gmask, sel_in);
 #pragma unroll
       for (int s = 0; s < STEPS; ++s) {
         // K = 1 << s, dispatched statically
-        if (s == 0) acc = Wd::addmax_relu(Wd::template shift<T, 1>(acc, t, gmask, sel[0]), NKD[0], acc);
-        if (s == 1) acc = Wd::addmax_relu(Wd::template shift<T, 2>(acc, t, gmask, sel[1]), NKD[1], acc);
-        if (s == 2) acc = Wd::addmax_relu(Wd::template shift<T, 4>(acc, t, gmask, sel[2]), NKD[2], acc);
-        if (s == 3) acc = Wd::addmax_relu(Wd::template shift<T, 8>(acc, t, gmask, sel[3]), NKD[3], acc);
-        if (s == 4) acc = Wd::addmax_relu(Wd::template shift<T, 16>(acc, t, gmask, sel[4]), NKD[4], acc);
+        if (s == 0) acc = Wd::addmax_relu(Wd::template scan_shift<T, 1>(acc, t, gmask, ssel[0]), NKD[0], acc);
+        if (s == 1) acc = Wd::addmax_relu(Wd::template scan_shift<T, 2>(acc, t, gmask, ssel[1]), NKD[1], acc);
+        if (s == 2) acc = Wd::addmax_relu(Wd::template scan_shift<T, 4>(acc, t, gmask, ssel[2]), NKD[2], acc);
+        if (s == 3) acc = Wd::addmax_relu(Wd::template scan_shift<T, 8>(acc, t, gmask, ssel[3]), NKD[3], acc);
+        if (s == 4) acc = Wd::addmax_relu(Wd::template scan_shift<T, 16>(acc, t, gmask, ssel[4]), NKD[4], acc);
         if constexpr (Wd::LPW == 2)
-          if (s == 5) acc = Wd::addmax_relu(Wd::template shift<T, 32>(acc, t, gmask, sel[5]), NKD[5], acc);
+          if (s == 5) acc = Wd::addmax_relu(Wd::template scan_shift<T, 32>(acc, t, gmask, ssel[5]), NKD[5], acc);
       }
-      carry = Wd::addmax(Wd::splat(fin), NLANE, acc);
+      carry = acc;  // includes the incoming F decayed by lane * L * ge
       wnext = Wd::addmax(carry, NWRAP, H[L - 1]);       // corrected H of the last word
       const uint32_t fo = Wd::addmax(carry, NLD, F);    // true F leaving each lane
       // the strip's last lane (thread 31, top half) holds this column's boundary

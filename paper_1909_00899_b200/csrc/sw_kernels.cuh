@@ -99,6 +99,27 @@ struct W16 {
   __device__ static __forceinline__ uint32_t shift_sel(int t, int k) {
     return t >= k ? 0x3210u : 0x1044u;  // r<<16: bytes {0,0,r0,r1}
   }
+  // scan shift: like shift, but source-less lanes keep their own value (bytes {v0,v1,r0,r1})
+  template <int T, int K>
+  __device__ static __forceinline__ uint32_t scan_shift(uint32_t v, int t, uint32_t gmask, uint32_t sel) {
+    if constexpr (K == T) {
+      return prmt(v, v, 0x1010u);  // {v.lo, v.lo}: low half keeps itself
+    } else {
+      uint32_t r = __shfl_sync(gmask, v, (t - K) & (T - 1), T);
+      return prmt(r, v, sel);
+    }
+  }
+  __device__ static __forceinline__ uint32_t scan_sel(int t, int k) {
+    return t >= k ? 0x3210u : 0x1054u;
+  }
+  // shift by one lane with `in` entering lane 0 (thread 0, low half)
+  template <int T>
+  __device__ static __forceinline__ uint32_t shift_in(uint32_t v, uint32_t in, int t, uint32_t gmask,
+                                                      uint32_t sel) {
+    uint32_t r = __shfl_sync(gmask, v, (t - 1) & (T - 1), T);
+    return prmt(r, in, sel);
+  }
+  __device__ static __forceinline__ uint32_t inject_sel(int t) { return t ? 0x3210u : 0x1054u; }
 };
 
 struct W32 {
@@ -128,6 +149,20 @@ struct W32 {
     return t >= K ? r : 0u;
   }
   __device__ static __forceinline__ uint32_t shift_sel(int, int) { return 0u; }
+  // scan shift: lanes t < K receive their own value (harmless in the max-plus step)
+  template <int T, int K>
+  __device__ static __forceinline__ uint32_t scan_shift(uint32_t v, int, uint32_t gmask, uint32_t) {
+    static_assert(K < T, "32-bit lanes shift inside the group");
+    return __shfl_up_sync(gmask, v, K, T);
+  }
+  __device__ static __forceinline__ uint32_t scan_sel(int, int) { return 0u; }
+  template <int T>
+  __device__ static __forceinline__ uint32_t shift_in(uint32_t v, uint32_t in, int t, uint32_t gmask,
+                                                      uint32_t) {
+    const uint32_t r = __shfl_up_sync(gmask, v, 1, T);
+    return t ? r : in;
+  }
+  __device__ static __forceinline__ uint32_t inject_sel(int) { return 0u; }
 };
 
 __host__ __device__ constexpr int ceil_log2(int p) {
@@ -640,4 +675,4 @@ SWB_X_DECL(4, 0, d) SWB_X_DECL(4, 1, d) SWB_X_DECL(4, 2, d)
 SWB_X_DECL(4, 0, e) SWB_X_DECL(4, 1, e) SWB_X_DECL(4, 2, e)
 SWB_X_DECL(4, 0, f) SWB_X_DECL(4, 1, f) SWB_X_DECL(4, 2, f)
 #undef SWB_X_DECL
-void swb_fill_chain(const void* (&tab)[2][4], const void* (&ptab)[2]);
+void swb_fill_chain(const void* (&tab)[2][6], const void* (&ptab)[2]);
