@@ -273,7 +273,7 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
                     const int64_t* d_start, const int32_t* d_len, const int32_t* d_order, int64_t n,
                     const int64_t* d_n_jobs, int32_t* d_score, int32_t* d_ref_end,
                     int32_t* d_query_end, uint8_t* d_flags, int32_t* d_col_passes,
-                    int64_t* d_pass_stats, sw_stream_t stream) {
+                    int64_t* d_pass_stats, const int32_t* d_coord_floor, sw_stream_t stream) {
   std::call_once(g_once, init_tables);
   if (!p || !d_prof || !d_tgt || !d_start || !d_len || !d_score)
     return fail(SW_EINVAL, "NULL argument");
@@ -321,6 +321,7 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
   a.flags = d_flags;
   a.col_passes = d_col_passes;
   a.pass_stats = d_pass_stats;
+  a.coord_floor = d_coord_floor;
   // exact instances stage the profile as [sym][ceil(L/4)][T][4]
   const size_t smem = block == 128 ? (size_t)(p->n_sym + 1) * ((p->seg_len + 3) / 4 * 4) * p->threads * 4
                                    : (size_t)p->prof_words * 4;

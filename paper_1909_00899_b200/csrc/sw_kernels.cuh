@@ -214,6 +214,7 @@ struct SwArgs {
   int64_t* pass_stats;       // optional [n_jobs][2]: total lazy-F passes, early-exit columns
   const int64_t* n_jobs_dev; // optional device-side job count (overrides n_jobs; rescue launches)
   int32_t pair_stride;       // pairs mode: words per group profile slice ((A+1)*Lmax*T)
+  const int32_t* coord_floor; // optional: locate end coordinates only for scores >= *floor
 };
 
 // ---- the striped kernel -----------------------------------------------------
@@ -325,6 +326,13 @@ sw_striped_kernel(const SwArgs a) {
   // pairs mode: each group owns a slice of (A+1)*LMAX*T words
   uint32_t* gslice = smem + (size_t)((threadIdx.x >> 5) * G + gw) * (size_t)a.pair_stride;
 
+  // Coordinate floor (database top-k): end coordinates are located only for
+  // alignments scoring >= *coord_floor, so the per-column gate compares against
+  // the floor and the thread's own best -- no group reduction per column.
+  const bool floor_mode = a.coord_floor != nullptr;
+  const int gb_init = floor_mode ? max(0, __ldg(a.coord_floor)) - 1 : 0;
+  constexpr int kCh = 8, kNch = (LMAX + kCh - 1) / kCh;
+
   for (int64_t task = warp_global; task < n_tasks; task += n_warps) {
     const int64_t slot = task * G + gw;
     const bool valid = slot < n_jobs;
@@ -381,8 +389,13 @@ sw_striped_kernel(const SwArgs a) {
     for (int c = 0; c < LMAX; ++c) { H[c] = 0u; E[c] = 0u; }
     uint32_t carry = 0u;
     int64_t tot_passes = 0, breaks = 0;  // lazy-F statistics (reference op counters)
-    int gb = 0;                       // best of all earlier columns, group-wide
+    int gb = gb_init;                 // best of all earlier columns (group-wide, or own + floor)
     int bv = 0, bcol = -1, bq = -1;   // this thread's first-maximum record
+    // running maxima of u per chunk of kCh words (never reset: a chunk reaches a
+    // value above gb only in the column that first produces it)
+    uint32_t cmk[kNch];
+#pragma unroll
+    for (int k = 0; k < kNch; ++k) cmk[k] = 0u;
     const int nullsym = A;
     int nxt = (len > 0) ? (int)__ldg(tp) : nullsym;
 
@@ -406,11 +419,6 @@ sw_striped_kernel(const SwArgs a) {
       if constexpr (VAR == VAR_SCAN) w = Wd::addmax(carry, NWRAP, w);
       uint32_t vh = Wd::template shift<T, 1>(w, t, cmask, sel[0]);
       uint32_t F = 0u;
-      // column maxima per chunk of kCh words: a position search only scans one chunk
-      constexpr int kCh = 8, kNch = (LMAX + kCh - 1) / kCh;
-      uint32_t cmk[kNch];
-#pragma unroll
-      for (int k = 0; k < kNch; ++k) cmk[k] = 0u;
 
 #define SWB_WORD_BODY(C)                                                   \
   {                                                                        \
@@ -481,7 +489,9 @@ sw_striped_kernel(const SwArgs a) {
           }
         }
       }
-      {
+      if (floor_mode) {
+        gb = max(gb, cmx);
+      } else {
         int g = max(gb, cmx);
 #pragma unroll
         for (int off = T / 2; off >= 1; off >>= 1) g = max(g, __shfl_xor_sync(cmask, g, off, T));
@@ -542,8 +552,16 @@ sw_striped_kernel(const SwArgs a) {
 
     // ---- reduce (best desc, ref_end asc, query_end asc) over the group ----
     int best = bv, col = bcol, q = bq;
+    int sc;  // the score: the running maximum (equals best unless the floor skipped it)
+    {
+      uint32_t cm = cmk[0];
+#pragma unroll
+      for (int k = 1; k < kNch; ++k) cm = Wd::vmax(cm, cmk[k]);
+      sc = Wd::hmax(cm);
+    }
 #pragma unroll
     for (int off = T / 2; off >= 1; off >>= 1) {
+      sc = max(sc, __shfl_xor_sync(gmask, sc, off, T));
       const int ob = __shfl_xor_sync(gmask, best, off, T);
       const int oc = __shfl_xor_sync(gmask, col, off, T);
       const int oq = __shfl_xor_sync(gmask, q, off, T);
@@ -554,12 +572,13 @@ sw_striped_kernel(const SwArgs a) {
     if (valid && t == 0) {
       uint8_t fl = 0;
       if constexpr (Wd::LPW == 2) {
-        if (best >= 32767 - max_sub) fl |= FLAG_RESCUE;
+        if (sc >= 32767 - max_sub) fl |= FLAG_RESCUE;
       }
-      if (best > 65535 - bias) fl |= FLAG_REF_OVERFLOW;
+      if (sc > 65535 - bias) fl |= FLAG_REF_OVERFLOW;
       if (a.n_jobs_dev) fl |= FLAG_RESCUED;  // device-counted launches are rescue passes
-      if (best == 0) { col = -1; q = -1; }
-      a.score[job] = best;
+      if (sc == 0) { col = -1; q = -1; }
+      else if (best != sc) { col = -2; q = -2; }  // below the coordinate floor: not located
+      a.score[job] = sc;
       if (a.pass_stats) {
         a.pass_stats[2 * job] = tot_passes;
         a.pass_stats[2 * job + 1] = breaks;

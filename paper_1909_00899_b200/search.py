@@ -104,12 +104,27 @@ class DatabaseSearch:
     current stream); ``align(query)`` runs profile build + 16-bit striped kernel
     + device-side 32-bit rescue; ``topk(k)`` returns the k best records of this
     rank as a device int64 tensor [k, 4] (score, target_id, ref_end, query_end).
+
+    ``coords``: ``"all"`` locates the end coordinates of every target;
+    ``"topk"`` locates them for every target that can enter the top ``k``: the
+    head of the database (the longest 1/16 of the targets, processed first) runs
+    with coordinates, the k-th best of its exact scores becomes a floor, and
+    the rest runs with ``d_coord_floor`` -- every target scoring >= the floor
+    (a superset of the final top k) gets exact coordinates, the others report
+    (-2, -2). Scores are exact in both modes.
     """
 
-    def __init__(self, scheme: ScoringScheme, kernel: str = "scan", lanes: int = 0):
+    HEAD_FRACTION = 16
+
+    def __init__(self, scheme: ScoringScheme, kernel: str = "scan", lanes: int = 0,
+                 coords: str = "all", k: int = 100):
+        if coords not in ("all", "topk"):
+            raise ValueError(f"coords must be 'all' or 'topk', got {coords!r}")
         self.scheme = scheme
         self.kernel = kernel
         self.lanes = lanes
+        self.coords = coords
+        self.k = k
         self.kid = _lib.KERNEL_IDS[kernel]
         self.dev: PackedDb | None = None
         self.out: dict | None = None
@@ -129,6 +144,7 @@ class DatabaseSearch:
                 "flags": torch.empty(n, dtype=torch.uint8, device="cuda"),
                 "_rescue": (torch.empty(max(n, 1), dtype=torch.int32, device="cuda"),
                             torch.zeros(1, dtype=torch.int64, device="cuda")),
+                "_floor": torch.zeros(1, dtype=torch.int32, device="cuda"),
             }
 
     def upload(self, packed: PackedDb) -> None:
@@ -153,17 +169,38 @@ class DatabaseSearch:
                                       _ptr(self.prof16), _stream()))
         self.launches += 1
 
-    def align(self) -> dict:
-        assert self.dev is not None and self.prof is not None, "upload() and set_query() first"
+    def _launch16(self, a: int, b: int, floor: bool) -> None:
+        """16-bit striped kernel over database slots [a, b) (outputs offset likewise)."""
+        L = _lib.load()
+        p, d, o, sch = self.prof, self.dev, self.out, self.scheme
+        ptr = lambda t, i: C.c_void_p(t.data_ptr() + i * t.element_size())  # noqa: E731
+        _lib.check(L.sw_db_align(C.byref(self.plan16), _ptr(self.prof16), self.kid, sch.gap_open,
+                                 sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes),
+                                 ptr(d.start, a), ptr(d.length, a), None, b - a, None,
+                                 ptr(o["score"], a), ptr(o["ref_end"], a),
+                                 ptr(o["query_end"], a), ptr(o["flags"], a), None, None,
+                                 _ptr(o["_floor"]) if floor else None, _stream()))
+        self.launches += 1
+
+    def _head(self, n: int) -> int:
+        """Slots [0, head) run with coordinates in coords='topk' mode (0: no split)."""
+        if self.coords != "topk":
+            return 0
+        head = max(self.k, n // self.HEAD_FRACTION)
+        return head if head < n else 0
+
+    def _set_floor(self, head: int) -> None:
+        """Floor = k-th best exact score of the head (16-bit results needing the
+        32-bit rescue are left out): a lower bound of the final k-th best."""
+        o = self.out
+        s = o["score"][:head].masked_fill((o["flags"][:head] & _lib.FLAG_RESCUE) != 0, 0)
+        kk = min(self.k, head)
+        o["_floor"].copy_(torch.topk(s, kk, sorted=False).values.min().reshape(1))
+
+    def _rescue(self, n: int) -> None:
         L = _lib.load()
         p, d, o, sch = self.prof, self.dev, self.out, self.scheme
         st = _stream()
-        n = d.n
-        _lib.check(L.sw_db_align(C.byref(self.plan16), _ptr(self.prof16), self.kid, sch.gap_open,
-                                 sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
-                                 _ptr(d.length), None, n, None, _ptr(o["score"]),
-                                 _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
-                                 None, None, st))
         lst, cnt = o["_rescue"]
         _lib.check(L.sw_collect_flagged(_ptr(o["flags"]), n, _lib.FLAG_RESCUE, _ptr(lst),
                                         _ptr(cnt), st))
@@ -171,9 +208,21 @@ class DatabaseSearch:
                                  sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
                                  _ptr(d.length), _ptr(lst), 0, _ptr(cnt), _ptr(o["score"]),
                                  _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
-                                 None, None, st))
-        self.launches += 3
-        return o
+                                 None, None, None, st))
+        self.launches += 2
+
+    def align(self) -> dict:
+        assert self.dev is not None and self.prof is not None, "upload() and set_query() first"
+        n = self.dev.n
+        head = self._head(n)
+        if head:
+            self._launch16(0, head, floor=False)
+            self._set_floor(head)
+            self._launch16(head, n, floor=True)
+        else:
+            self._launch16(0, n, floor=False)
+        self._rescue(n)
+        return self.out
 
     def search_streamed(self, packed: PackedDb, n_chunks: int = 8) -> dict:
         """End-to-end form for a host-resident (pinned) database: chunk k+1 is
@@ -181,8 +230,7 @@ class DatabaseSearch:
         hides behind compute. Requires set_query(); returns the result dict."""
         assert self.prof is not None, "set_query() first"
         self._ensure_buffers(packed)
-        L = _lib.load()
-        d, o, p, sch = self.dev, self.out, self.prof, self.scheme
+        d, o = self.dev, self.out
         n = packed.n
         cur = torch.cuda.current_stream()
         copy = self._copy_stream = getattr(self, "_copy_stream", None) or torch.cuda.Stream()
@@ -202,27 +250,23 @@ class DatabaseSearch:
                 ev = torch.cuda.Event()
                 ev.record(copy)
             events.append((a, b, ev))
-        st = _stream()
+        head = self._head(n)
+        floor_set = False
         for a, b, ev in events:
             cur.wait_event(ev)
             if b <= a:
                 continue
-            ptr = lambda t, i: C.c_void_p(t.data_ptr() + i * t.element_size())  # noqa: E731
-            _lib.check(L.sw_db_align(C.byref(self.plan16), _ptr(self.prof16), self.kid, sch.gap_open,
-                                     sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes),
-                                     ptr(d.start, a), ptr(d.length, a), None, b - a, None,
-                                     ptr(o["score"], a), ptr(o["ref_end"], a),
-                                     ptr(o["query_end"], a), ptr(o["flags"], a), None, None, st))
-            self.launches += 1
-        lst, cnt = o["_rescue"]
-        _lib.check(L.sw_collect_flagged(_ptr(o["flags"]), n, _lib.FLAG_RESCUE, _ptr(lst),
-                                        _ptr(cnt), st))
-        _lib.check(L.sw_db_align(C.byref(p.plan32), _ptr(p.prof32), self.kid, sch.gap_open,
-                                 sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
-                                 _ptr(d.length), _ptr(lst), 0, _ptr(cnt), _ptr(o["score"]),
-                                 _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
-                                 None, None, st))
-        self.launches += 2
+            if head and not floor_set and a >= head:
+                self._set_floor(head)
+                floor_set = True
+            if head and a < head < b:  # the head boundary splits this chunk
+                self._launch16(a, head, floor=False)
+                self._set_floor(head)
+                floor_set = True
+                self._launch16(head, b, floor=True)
+            else:
+                self._launch16(a, b, floor=floor_set)
+        self._rescue(n)
         return o
 
     def topk(self, k: int = 100) -> torch.Tensor:

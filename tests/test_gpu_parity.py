@@ -182,6 +182,71 @@ def test_config2_subset_db(A, oracle):
         assert (out["score"].cpu().numpy() == sc).all(), p
 
 
+def test_coordinate_floor_db(A, oracle):
+    """d_coord_floor: scores stay exact for every target; end coordinates equal the
+    oracle's for scores >= floor, (-2, -2) below it, (-1, -1) for score 0."""
+    import ctypes as C
+
+    import torch as T
+
+    from paper_1909_00899_b200 import _lib, workloads as W
+    from paper_1909_00899_b200.align import _ptr, _stream
+
+    w = W.config2(n_targets=600)
+    sc, rend, qend = oracle.db_scalar(w.query, w.db, w.offsets, w.scheme.as_array(), 11, 1)
+    prof = A.build_profile_arrays(w.query, w.scheme)
+    plan16, prof16 = prof.for_kernel("scan")
+    tgt = T.from_numpy(w.db).cuda()
+    start = T.from_numpy(w.offsets[:-1].copy()).cuda()
+    length = T.from_numpy(np.diff(w.offsets).astype(np.int32)).cuda()
+    n = w.n_targets
+    for floor in (0, 1, int(np.median(sc)), int(np.percentile(sc, 90)), int(sc.max()),
+                  int(sc.max()) + 1):
+        o = {k: T.full((n,), -7, dtype=T.int32, device="cuda") for k in ("s", "r", "q")}
+        fl = T.empty(n, dtype=T.uint8, device="cuda")
+        fv = T.tensor([floor], dtype=T.int32, device="cuda")
+        _lib.check(_lib.load().sw_db_align(C.byref(plan16), _ptr(prof16), 2, 11, 1, prof.bias,
+                                           prof.max_sub, _ptr(tgt), _ptr(start), _ptr(length),
+                                           None, n, None, _ptr(o["s"]), _ptr(o["r"]),
+                                           _ptr(o["q"]), _ptr(fl), None, None, _ptr(fv),
+                                           _stream()))
+        s_, r_, q_ = (o[k].cpu().numpy() for k in ("s", "r", "q"))
+        assert (s_ == sc).all(), floor
+        located = (sc >= floor) & (sc > 0)
+        assert (r_[located] == rend[located]).all() and (q_[located] == qend[located]).all()
+        skipped = (sc < floor) & (sc > 0)
+        assert (r_[skipped] == -2).all() and (q_[skipped] == -2).all()
+        assert (r_[sc == 0] == -1).all() and (q_[sc == 0] == -1).all()
+
+
+def test_database_search_topk_coords(A):
+    """coords='topk' (floor from the database head) returns the same scores as
+    coords='all' everywhere and the same top-k records, coordinates included."""
+    from paper_1909_00899_b200 import search, workloads as W
+
+    w = W.config2(n_targets=40000)
+    packed = search.pack(w.db, w.offsets, pin=False)
+    res = {}
+    for mode in ("all", "topk"):
+        eng = search.DatabaseSearch(w.scheme, coords=mode, k=100)
+        eng.upload(packed)
+        eng.set_query(w.query)
+        o = eng.align()
+        res[mode] = ({k: o[k].cpu().numpy() for k in ("score", "ref_end", "query_end")},
+                     eng.topk(100).cpu().numpy())
+        streamed = eng.search_streamed(packed, n_chunks=16)
+        assert (streamed["score"].cpu().numpy() == res[mode][0]["score"]).all()
+        assert (eng.topk(100).cpu().numpy() == res[mode][1]).all(), mode
+    a, t = res["all"][0], res["topk"][0]
+    assert (a["score"] == t["score"]).all()
+    assert (res["all"][1] == res["topk"][1]).all()
+    assert (res["topk"][1][:, 2:] >= 0).all()  # every top hit is located
+    got = t["ref_end"] != -2
+    assert (t["ref_end"][got] == a["ref_end"][got]).all()
+    assert (t["query_end"][got] == a["query_end"][got]).all()
+    assert got.sum() < 0.5 * got.size  # the floor skipped most of the database
+
+
 def test_config3_subset_pairs(A, oracle):
     from paper_1909_00899_b200 import workloads as W
 
@@ -380,7 +445,7 @@ def test_config2_full_database_properties(A, oracle):
                                        prof.bias, prof.max_sub, _ptr(tgt), _ptr(start),
                                        _ptr(length), None, n, None, _ptr(o32["score"]),
                                        _ptr(o32["ref_end"]), _ptr(o32["query_end"]), _ptr(fl),
-                                       None, None, _stream()))
+                                       None, None, None, _stream()))
     for k in ("score", "ref_end", "query_end"):
         assert (o32[k].cpu().numpy() == res["scan"][k]).all(), k
     rng = np.random.default_rng(0xD0B)
