@@ -323,7 +323,9 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
   a.pass_stats = d_pass_stats;
   a.coord_floor = d_coord_floor;
   // exact instances stage the profile as [sym][ceil(L/4)][T][4]
-  const size_t smem = block == 128 ? (size_t)(p->n_sym + 1) * ((p->seg_len + 3) / 4 * 4) * p->threads * 4
+  // (T = 4: two copies at 32-word block granularity, see DUP in sw_kernels.cuh)
+  const size_t smem = block == 128 ? (size_t)(p->n_sym + 1) * ((p->seg_len + 3) / 4 * 4) * p->threads * 4 *
+                                         (p->threads == 4 ? 2 : 1)
                                    : (size_t)p->prof_words * 4;
   const int G = 32 / p->threads;
   const int64_t tasks = d_n_jobs ? 0 : (n + G - 1) / G;

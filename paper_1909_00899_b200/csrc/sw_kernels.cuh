@@ -247,6 +247,12 @@ sw_striped_kernel(const SwArgs a) {
   constexpr int G = 32 / T;
   constexpr bool VEC = EXACT;          // vectorised [sym][L/4][T][4] profile layout
   constexpr int LP4 = (LMAX + 3) / 4;
+  // With T = 4 a (sym, j4) block is 16 words = half the banks, and the two groups
+  // of a quarter-warp LDS.128 phase read different symbols: blocks are placed at
+  // 32-word granularity with the group parity selecting the half, so the phase
+  // never conflicts (DB mode: two copies; pairs mode: two groups interleaved).
+  constexpr bool DUP = VEC && T == 4;
+  constexpr int BW = DUP ? 32 : T * 4;  // words per (sym, j4) block
 
   extern __shared__ uint32_t smem[];
 
@@ -299,16 +305,15 @@ sw_striped_kernel(const SwArgs a) {
     first = LMAX - L;
     LT = L * T;
     if constexpr (VEC) {
-      // [(A+1)][L/4][T][4]: a thread's 4 consecutive words are one 16-byte LDS and
-      // a group (quarter warp) reads 128 contiguous bytes: no bank conflicts
-      // between the groups of a warp, which read different symbol rows.
-      const int words = (A + 1) * LP4 * T * 4;
+      // [(A+1)][L/4][copy][T][4]: a thread's 4 consecutive words are one 16-byte
+      // LDS; a group reads 4*T contiguous words of its symbol row.
+      const int words = (A + 1) * LP4 * BW;
       for (int w = threadIdx.x; w < words; w += blockDim.x) {
-        const int k = w & 3, tt = (w >> 2) % T, j4 = (w / (4 * T)) % LP4, sym = w / (4 * T * LP4);
+        const int k = w & 3, tt = (w >> 2) % T, j4 = (w / BW) % LP4, sym = w / (BW * LP4);
         const int j = 4 * j4 + k;
         smem[w] = j < L ? __ldg(a.prof + (sym * L + j) * T + tt) : 0u;
       }
-      LT = LP4 * T * 4;
+      LT = LP4 * BW;
     } else {
       const int words = (A + 1) * LT;
       const uint4* src = reinterpret_cast<const uint4*>(a.prof);
@@ -318,13 +323,15 @@ sw_striped_kernel(const SwArgs a) {
     }
     __syncthreads();
     set_gaps(a.go, a.ge, L);
-    prof_base = VEC ? smem + 4 * t : smem + t - first * T;
+    prof_base = VEC ? smem + 4 * t + (DUP ? 16 * (gw & 1) : 0) : smem + t - first * T;
   } else {
     LT = 0;
     prof_base = nullptr;
   }
   // pairs mode: each group owns a slice of (A+1)*LMAX*T words
-  uint32_t* gslice = smem + (size_t)((threadIdx.x >> 5) * G + gw) * (size_t)a.pair_stride;
+  uint32_t* gslice =
+      DUP ? smem + (size_t)((threadIdx.x >> 5) * G + (gw & ~1)) * (size_t)a.pair_stride + 16 * (gw & 1)
+          : smem + (size_t)((threadIdx.x >> 5) * G + gw) * (size_t)a.pair_stride;
 
   // Coordinate floor (database top-k): end coordinates are located only for
   // alignments scoring >= *coord_floor, so the per-column gate compares against
@@ -373,12 +380,12 @@ sw_striped_kernel(const SwArgs a) {
             v[h] = s;
           }
           if constexpr (VEC)
-            gslice[((sym * LP4 + (j >> 2)) * T + t) * 4 + (j & 3)] = Wd::pack(v[0], v[1]);
+            gslice[(sym * LP4 + (j >> 2)) * BW + t * 4 + (j & 3)] = Wd::pack(v[0], v[1]);
           else
             gslice[(sym * L + j) * T + t] = Wd::pack(v[0], v[1]);
         }
       }
-      if constexpr (VEC) LT = LP4 * T * 4;
+      if constexpr (VEC) LT = LP4 * BW;
       prof_base = VEC ? gslice + 4 * t : gslice + t - first * T;
     }
     const int maxlen = __reduce_max_sync(0xffffffffu, len);
@@ -407,7 +414,7 @@ sw_striped_kernel(const SwArgs a) {
       uint4 S4[VEC ? LP4 : 1];
       if constexpr (VEC) {
 #pragma unroll
-        for (int k = 0; k < LP4; ++k) S4[k] = *reinterpret_cast<const uint4*>(pr + k * T * 4);
+        for (int k = 0; k < LP4; ++k) S4[k] = *reinterpret_cast<const uint4*>(pr + k * BW);
       }
 
       // scan path: the whole warp is converged here, so shuffles take the full
