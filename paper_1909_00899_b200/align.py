@@ -257,10 +257,11 @@ def align_long(query, ref, scheme: ScoringScheme, width: int = 32, kernel: str =
 def db_align(prof: DeviceProfile, tgt: torch.Tensor, start: torch.Tensor, length: torch.Tensor,
              order: torch.Tensor | None = None, kernel: str = "scan",
              col_passes: torch.Tensor | None = None, out: dict | None = None,
-             rescue: bool = True) -> dict:
+             rescue: bool = True, coord_floor: torch.Tensor | None = None) -> dict:
     """All-device database alignment: one profile vs n targets, 16-bit with a
     device-side 32-bit rescue of wrap-guard hits. Returns dict of device tensors
-    ``score, ref_end, query_end, flags`` indexed by target id."""
+    ``score, ref_end, query_end, flags`` indexed by target id. ``coord_floor``
+    (device int32 [1]): locate end coordinates only for scores >= the floor."""
     L = _lib.load()
     n = int(length.shape[0])
     if out is None:
@@ -278,7 +279,7 @@ def db_align(prof: DeviceProfile, tgt: torch.Tensor, start: torch.Tensor, length
                              sch.gap_extend, prof.bias, prof.max_sub, _ptr(tgt), _ptr(start),
                              _ptr(length), _ptr(order), n, None, _ptr(out["score"]),
                              _ptr(out["ref_end"]), _ptr(out["query_end"]), _ptr(out["flags"]),
-                             _ptr(col_passes), None, None, st))
+                             _ptr(col_passes), None, _ptr(coord_floor), st))
     if rescue:
         _rescue_db(prof, tgt, start, length, kid, col_passes, out, n)
     return out

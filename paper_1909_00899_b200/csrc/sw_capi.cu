@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 
 #include "sw_chain.cuh"
@@ -137,9 +138,40 @@ int plan(int m, int n_sym, int width, int lanes, sw_plan_t* out) {
   return SW_OK;
 }
 
-int launch(const void* fn, const SwArgs& args, size_t smem, int block, int64_t n_tasks_hint,
+// Task counters for dynamic task claiming (SwArgs::task_ctr): one 128-byte line per
+// slot, kCtrSlots slots per device allocated once (128 KB); each launch takes the
+// next slot and zeroes it on its stream, so launches on different streams do not
+// share a counter.
+constexpr int kCtrSlots = 1024;
+constexpr int kMaxDev = 64;
+std::mutex g_ctr_mu;
+unsigned long long* g_ctr[kMaxDev] = {};
+std::atomic<uint32_t> g_ctr_next{0};
+
+cudaError_t task_counter(cudaStream_t stream, unsigned long long** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+  {
+    std::lock_guard<std::mutex> lk(g_ctr_mu);
+    if (!g_ctr[dev]) {
+      e = cudaMalloc((void**)&g_ctr[dev], (size_t)kCtrSlots * 128);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  unsigned long long* p = g_ctr[dev] + (size_t)(g_ctr_next++ % kCtrSlots) * 16;
+  e = cudaMemsetAsync(p, 0, sizeof(unsigned long long), stream);
+  *out = p;
+  return e;
+}
+
+int launch(const void* fn, const SwArgs& args_in, size_t smem, int block, int64_t n_tasks_hint,
            cudaStream_t stream) {
   cudaError_t e;
+  SwArgs args = args_in;
+  e = task_counter(stream, &args.task_ctr);
+  if (e != cudaSuccess) return cuda_fail(e, "task counter");
   if (smem > 48 * 1024) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(smem)");

@@ -215,6 +215,7 @@ struct SwArgs {
   const int64_t* n_jobs_dev; // optional device-side job count (overrides n_jobs; rescue launches)
   int32_t pair_stride;       // pairs mode: words per group profile slice ((A+1)*Lmax*T)
   const int32_t* coord_floor; // optional: locate end coordinates only for scores >= *floor
+  unsigned long long* task_ctr; // optional zeroed counter: warps claim tasks dynamically
 };
 
 // ---- the striped kernel -----------------------------------------------------
@@ -340,7 +341,20 @@ sw_striped_kernel(const SwArgs a) {
   const int gb_init = floor_mode ? max(0, __ldg(a.coord_floor)) - 1 : 0;
   constexpr int kCh = 8, kNch = (LMAX + kCh - 1) / kCh;
 
-  for (int64_t task = warp_global; task < n_tasks; task += n_warps) {
+  // Task claiming: with a counter, warps take the next task (in length-descending
+  // order) when they finish one -- longest-first greedy, so the warps end together
+  // instead of the static stride leaving the warps that drew the longest targets
+  // of every round running alone at the end. The next claim is issued at the top
+  // of each task so the atomic's latency hides behind the alignment.
+  auto claim = [&]() -> int64_t {
+    unsigned long long v = 0;
+    if (lane == 0) v = atomicAdd(a.task_ctr, 1ull);
+    return (int64_t)v;
+  };
+  int64_t task = a.task_ctr ? (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)claim(), 0)
+                            : warp_global;
+  while (task < n_tasks) {
+    const int64_t pref = a.task_ctr ? claim() : task + n_warps;
     const int64_t slot = task * G + gw;
     const bool valid = slot < n_jobs;
     const int64_t job = valid ? (a.order ? (int64_t)a.order[slot] : slot) : 0;
@@ -594,6 +608,7 @@ sw_striped_kernel(const SwArgs a) {
       if (a.query_end) a.query_end[job] = q;
       if (a.flags) a.flags[job] = fl;
     }
+    task = a.task_ctr ? (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)pref, 0) : pref;
   }
 }
 

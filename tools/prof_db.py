@@ -20,6 +20,8 @@ def main() -> None:
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--lanes", type=int, default=0)
     ap.add_argument("--kernel", default="scan")
+    ap.add_argument("--floor-topk", type=int, default=0,
+                    help="after one full run, use the k-th best score as the coordinate floor")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -34,10 +36,16 @@ def main() -> None:
     order = torch.from_numpy(np.argsort(-np.diff(w.offsets), kind="stable").astype(np.int32)).cuda()
     cells = w.cells
     print("plan", prof.plan16)
+    floor = None
+    if args.floor_topk:
+        o = align.db_align(prof, tgt, start, length, order, args.kernel, rescue=False)
+        floor = torch.topk(o["score"], args.floor_topk).values.min().reshape(1).to(torch.int32)
+        print("coordinate floor", int(floor.item()))
     for _ in range(args.reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        align.db_align(prof, tgt, start, length, order, args.kernel, rescue=False)
+        align.db_align(prof, tgt, start, length, order, args.kernel, rescue=False,
+                       coord_floor=floor)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
