@@ -263,7 +263,7 @@ def main() -> None:
                                  w.scheme.gap_extend, p.bias, p.max_sub, _ptr(d.codes),
                                  _ptr(d.start), _ptr(d.length), None, d.n, None,
                                  _ptr(o["score"]), _ptr(o["ref_end"]), _ptr(o["query_end"]),
-                                 _ptr(o["flags"]), None, None, _ptr(o["_floor"]), _stream()))
+                                 _ptr(o["flags"]), None, None, _ptr(o["_floor"]), 0, 0, _stream()))
     ek1.record(stream)
     torch.cuda.synchronize()
     k_ms = ek0.elapsed_time(ek1) / k_reps

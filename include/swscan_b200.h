@@ -92,14 +92,19 @@ int32_t sw_profile_build(const sw_plan_t* plan, const uint8_t* d_query, const in
  * d_coord_floor (nullable device int32): end coordinates are located only for
  * alignments scoring >= *d_coord_floor (others report ref_end = query_end = -2;
  * scores are always exact).  A database search passes a lower bound of its
- * top-k threshold so that only candidate hits pay for the position search. */
+ * top-k threshold so that only candidate hits pay for the position search.
+ * floor_sample > 0 (16-bit plans): the kernel itself raises *d_coord_floor (which
+ * must hold a valid floor at launch, e.g. 0) to the floor_k-th best exact score of
+ * the first floor_sample jobs in processing order once they complete -- a lower
+ * bound of the final top-floor_k threshold, found without a second launch. */
 int32_t sw_db_align(const sw_plan_t* plan, const uint32_t* d_prof, int32_t kernel,
                     int32_t gap_open, int32_t gap_extend, int32_t bias, int32_t max_sub,
                     const uint8_t* d_tgt, const int64_t* d_start, const int32_t* d_len,
                     const int32_t* d_order, int64_t n, const int64_t* d_n_jobs,
                     int32_t* d_score, int32_t* d_ref_end, int32_t* d_query_end, uint8_t* d_flags,
                     int32_t* d_col_passes, int64_t* d_pass_stats,
-                    const int32_t* d_coord_floor, sw_stream_t stream);
+                    int32_t* d_coord_floor, int64_t floor_sample, int32_t floor_k,
+                    sw_stream_t stream);
 
 /* n independent (query_k, target_k) pairs.  Reference: batch_align(kernel_id, p,
  * flat_q, q_off, flat_r, r_off, match_a, mis_a, go_a, ge_a), src/_compiled.py:504-529.

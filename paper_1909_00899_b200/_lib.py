@@ -104,7 +104,7 @@ def load():
     L.sw_profile_build.argtypes = [C.POINTER(Plan), vp, vp, i32, vp, vp]
     L.sw_db_align.restype = i32
     L.sw_db_align.argtypes = [C.POINTER(Plan), vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, i64,
-                              vp, vp, vp, vp, vp, vp, vp, vp, vp]
+                              vp, vp, vp, vp, vp, vp, vp, vp, i64, i32, vp]
     L.sw_pairs_align.restype = i32
     L.sw_pairs_align.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, vp, i32, i32, vp, i32,
                                  i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]

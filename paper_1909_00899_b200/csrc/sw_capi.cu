@@ -138,17 +138,19 @@ int plan(int m, int n_sym, int width, int lanes, sw_plan_t* out) {
   return SW_OK;
 }
 
-// Task counters for dynamic task claiming (SwArgs::task_ctr): one 128-byte line per
-// slot, kCtrSlots slots per device allocated once (128 KB); each launch takes the
-// next slot and zeroes it on its stream, so launches on different streams do not
-// share a counter.
-constexpr int kCtrSlots = 1024;
+// Task counters for dynamic task claiming (SwArgs::task_ctr) and the coordinate-floor
+// sample histogram: one slot = a 128-byte counter line + kFloorBins words, kCtrSlots
+// slots per device allocated once (~1 MB); each launch takes the next slot and zeroes
+// what it uses on its stream, so launches on different streams do not share a slot.
+constexpr int kCtrSlots = 64;
+constexpr size_t kSlotBytes = 128 + kFloorBins * 4;
 constexpr int kMaxDev = 64;
 std::mutex g_ctr_mu;
 unsigned long long* g_ctr[kMaxDev] = {};
 std::atomic<uint32_t> g_ctr_next{0};
 
-cudaError_t task_counter(cudaStream_t stream, unsigned long long** out) {
+cudaError_t task_counter(cudaStream_t stream, bool hist, unsigned long long** out,
+                         uint32_t** hist_out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -156,13 +158,14 @@ cudaError_t task_counter(cudaStream_t stream, unsigned long long** out) {
   {
     std::lock_guard<std::mutex> lk(g_ctr_mu);
     if (!g_ctr[dev]) {
-      e = cudaMalloc((void**)&g_ctr[dev], (size_t)kCtrSlots * 128);
+      e = cudaMalloc((void**)&g_ctr[dev], (size_t)kCtrSlots * kSlotBytes);
       if (e != cudaSuccess) return e;
     }
   }
-  unsigned long long* p = g_ctr[dev] + (size_t)(g_ctr_next++ % kCtrSlots) * 16;
-  e = cudaMemsetAsync(p, 0, sizeof(unsigned long long), stream);
-  *out = p;
+  char* slot = (char*)g_ctr[dev] + (size_t)(g_ctr_next++ % kCtrSlots) * kSlotBytes;
+  e = cudaMemsetAsync(slot, 0, hist ? kSlotBytes : 2 * sizeof(unsigned long long), stream);
+  *out = (unsigned long long*)slot;
+  *hist_out = (uint32_t*)(slot + 128);
   return e;
 }
 
@@ -170,7 +173,7 @@ int launch(const void* fn, const SwArgs& args_in, size_t smem, int block, int64_
            cudaStream_t stream) {
   cudaError_t e;
   SwArgs args = args_in;
-  e = task_counter(stream, &args.task_ctr);
+  e = task_counter(stream, args.floor_sample > 0, &args.task_ctr, &args.floor_hist);
   if (e != cudaSuccess) return cuda_fail(e, "task counter");
   if (smem > 48 * 1024) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -305,7 +308,8 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
                     const int64_t* d_start, const int32_t* d_len, const int32_t* d_order, int64_t n,
                     const int64_t* d_n_jobs, int32_t* d_score, int32_t* d_ref_end,
                     int32_t* d_query_end, uint8_t* d_flags, int32_t* d_col_passes,
-                    int64_t* d_pass_stats, const int32_t* d_coord_floor, sw_stream_t stream) {
+                    int64_t* d_pass_stats, int32_t* d_coord_floor, int64_t floor_sample,
+                    int32_t floor_k, sw_stream_t stream) {
   std::call_once(g_once, init_tables);
   if (!p || !d_prof || !d_tgt || !d_start || !d_len || !d_score)
     return fail(SW_EINVAL, "NULL argument");
@@ -353,7 +357,13 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
   a.flags = d_flags;
   a.col_passes = d_col_passes;
   a.pass_stats = d_pass_stats;
+  if (floor_sample > 0 && (!d_coord_floor || floor_k < 1))
+    return fail(SW_EINVAL, "floor_sample needs d_coord_floor and floor_k >= 1");
+  if (floor_sample > 0 && p->width != 16)
+    return fail(SW_ENOTSUP, "the sampled coordinate floor is for 16-bit launches");
   a.coord_floor = d_coord_floor;
+  a.floor_sample = floor_sample;
+  a.floor_k = floor_k;
   // exact instances stage the profile as [sym][ceil(L/4)][T][4]
   // (T = 4: two copies at 32-word block granularity, see DUP in sw_kernels.cuh)
   const size_t smem = block == 128 ? (size_t)(p->n_sym + 1) * ((p->seg_len + 3) / 4 * 4) * p->threads * 4 *

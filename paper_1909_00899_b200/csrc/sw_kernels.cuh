@@ -214,9 +214,13 @@ struct SwArgs {
   int64_t* pass_stats;       // optional [n_jobs][2]: total lazy-F passes, early-exit columns
   const int64_t* n_jobs_dev; // optional device-side job count (overrides n_jobs; rescue launches)
   int32_t pair_stride;       // pairs mode: words per group profile slice ((A+1)*Lmax*T)
-  const int32_t* coord_floor; // optional: locate end coordinates only for scores >= *floor
-  unsigned long long* task_ctr; // optional zeroed counter: warps claim tasks dynamically
+  int32_t* coord_floor;       // optional: locate end coordinates only for scores >= *floor
+  int64_t floor_sample;       // > 0: raise *coord_floor to the floor_k-th best exact score
+  int32_t floor_k;            //      of the first floor_sample jobs once they complete
+  unsigned long long* task_ctr; // optional zeroed counters: [0] task claims, [1] sample tasks done
+  uint32_t* floor_hist;       // zeroed [kFloorBins] histogram of the sample's scores
 };
+constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095 share the top bin)
 
 // ---- the striped kernel -----------------------------------------------------
 #define SWB_REP32(X)                                                                     \
@@ -336,9 +340,10 @@ sw_striped_kernel(const SwArgs a) {
 
   // Coordinate floor (database top-k): end coordinates are located only for
   // alignments scoring >= *coord_floor, so the per-column gate compares against
-  // the floor and the thread's own best -- no group reduction per column.
-  const bool floor_mode = a.coord_floor != nullptr;
-  const int gb_init = floor_mode ? max(0, __ldg(a.coord_floor)) - 1 : 0;
+  // the floor and the thread's own best -- no group reduction per column. A floor
+  // of 0 (not yet raised by the sample) keeps the group-wide gate.
+  const bool has_floor = a.coord_floor != nullptr;
+  const int64_t fs_tasks = (has_floor && a.task_ctr) ? min((a.floor_sample + G - 1) / G, n_tasks) : 0;
   constexpr int kCh = 8, kNch = (LMAX + kCh - 1) / kCh;
 
   // Task claiming: with a counter, warps take the next task (in length-descending
@@ -410,7 +415,15 @@ sw_striped_kernel(const SwArgs a) {
     for (int c = 0; c < LMAX; ++c) { H[c] = 0u; E[c] = 0u; }
     uint32_t carry = 0u;
     int64_t tot_passes = 0, breaks = 0;  // lazy-F statistics (reference op counters)
-    int gb = gb_init;                 // best of all earlier columns (group-wide, or own + floor)
+    // best of all earlier columns: group-wide, or (floor mode) own best and floor - 1;
+    // the floor is re-read per task, as a sample-complete warp may have raised it
+    int floor_v = 0;
+    if (has_floor) {
+      if (lane == 0) floor_v = *(volatile const int32_t*)a.coord_floor;
+      floor_v = __shfl_sync(0xffffffffu, floor_v, 0);
+    }
+    const bool floor_mode = floor_v > 0;
+    int gb = floor_mode ? floor_v - 1 : 0;
     int bv = 0, bcol = -1, bq = -1;   // this thread's first-maximum record
     // running maxima of u per chunk of kCh words (never reset: a chunk reaches a
     // value above gb only in the column that first produces it)
@@ -607,6 +620,52 @@ sw_striped_kernel(const SwArgs a) {
       if (a.ref_end) a.ref_end[job] = col;
       if (a.query_end) a.query_end[job] = q;
       if (a.flags) a.flags[job] = fl;
+      if (task < fs_tasks)  // sample histogram (16-bit rescue candidates count as 0)
+        atomicAdd(a.floor_hist + min((fl & FLAG_RESCUE) ? 0 : sc, kFloorBins - 1), 1u);
+    }
+    if (task < fs_tasks) {
+      // the warp completing the last sample task sets the floor: the floor_k-th best
+      // exact score of the sample (capped at kFloorBins-1), a lower bound of the
+      // final k-th best, so every possible top-k hit is located
+      __threadfence();
+      __syncwarp();
+      unsigned long long done = 0;
+      if (lane == 0) done = atomicAdd(a.task_ctr + 1, 1ull);
+      done = __shfl_sync(0xffffffffu, done, 0);
+      if ((int64_t)done == fs_tasks - 1) {
+        __threadfence();
+        // one lane scans the histogram from the top, 32 bins per step (warp
+        // collectives here would raise the register allocation of the whole kernel)
+        int floor_v = 0;
+        if (lane == 0) {
+          const uint4* h4 = reinterpret_cast<const uint4*>(a.floor_hist);
+          int acc = 0;
+          for (int q = kFloorBins / 4 - 8; q >= 0; q -= 8) {
+            uint4 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = __ldcg(h4 + q + j);
+            int tot = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) tot += (int)(v[j].x + v[j].y + v[j].z + v[j].w);
+            if (acc + tot >= a.floor_k) {
+              int f = -1;  // the highest bin at which the count from the top reaches k
+#pragma unroll
+              for (int j = 7; j >= 0; --j) {
+                const int c[4] = {(int)v[j].x, (int)v[j].y, (int)v[j].z, (int)v[j].w};
+#pragma unroll
+                for (int e = 3; e >= 0; --e) {
+                  acc += c[e];
+                  if (acc >= a.floor_k && f < 0) f = 4 * (q + j) + e;
+                }
+              }
+              floor_v = f;
+              break;
+            }
+            acc += tot;
+          }
+        }
+        if (lane == 0) atomicMax(a.coord_floor, floor_v);
+      }
     }
     task = a.task_ctr ? (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)pref, 0) : pref;
   }

@@ -107,14 +107,16 @@ class DatabaseSearch:
 
     ``coords``: ``"all"`` locates the end coordinates of every target;
     ``"topk"`` locates them for every target that can enter the top ``k``: the
-    head of the database (the longest 1/16 of the targets, processed first) runs
-    with coordinates, the k-th best of its exact scores becomes a floor, and
-    the rest runs with ``d_coord_floor`` -- every target scoring >= the floor
-    (a superset of the final top k) gets exact coordinates, the others report
-    (-2, -2). Scores are exact in both modes.
+    launch processes a strided sample of the database first (every 16th target
+    outside the longest 1/8, so the sample finishes quickly), and the warp that
+    completes the sample raises a coordinate floor to the k-th best of its
+    exact scores (``floor_sample`` of ``sw_db_align``); every later task reads
+    the floor. Every target scoring >= the floor (a superset of the final top
+    k) gets exact coordinates, the others report (-2, -2). Scores are exact in
+    both modes. One launch, no host sync.
     """
 
-    HEAD_FRACTION = 16
+    SAMPLE_STRIDE = 16
 
     def __init__(self, scheme: ScoringScheme, kernel: str = "scan", lanes: int = 0,
                  coords: str = "all", k: int = 100):
@@ -169,33 +171,42 @@ class DatabaseSearch:
                                       _ptr(self.prof16), _stream()))
         self.launches += 1
 
-    def _launch16(self, a: int, b: int, floor: bool) -> None:
-        """16-bit striped kernel over database slots [a, b) (outputs offset likewise)."""
+    def _launch16(self, a: int, b: int, floor: bool, sample: int = 0,
+                  order: torch.Tensor | None = None) -> None:
+        """16-bit striped kernel over database slots [a, b) (outputs offset likewise);
+        ``order``: processing order of the local job ids 0..b-a-1; ``floor``: gate
+        coordinates on the floor buffer; ``sample`` > 0: the launch raises the floor
+        from the first ``sample`` jobs of its processing order (see sw_db_align)."""
         L = _lib.load()
         p, d, o, sch = self.prof, self.dev, self.out, self.scheme
         ptr = lambda t, i: C.c_void_p(t.data_ptr() + i * t.element_size())  # noqa: E731
         _lib.check(L.sw_db_align(C.byref(self.plan16), _ptr(self.prof16), self.kid, sch.gap_open,
                                  sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes),
-                                 ptr(d.start, a), ptr(d.length, a), None, b - a, None,
+                                 ptr(d.start, a), ptr(d.length, a), _ptr(order), b - a, None,
                                  ptr(o["score"], a), ptr(o["ref_end"], a),
                                  ptr(o["query_end"], a), ptr(o["flags"], a), None, None,
-                                 _ptr(o["_floor"]) if floor else None, _stream()))
+                                 _ptr(o["_floor"]) if floor else None, sample, self.k,
+                                 _stream()))
         self.launches += 1
 
-    def _head(self, n: int) -> int:
-        """Slots [0, head) run with coordinates in coords='topk' mode (0: no split)."""
-        if self.coords != "topk":
-            return 0
-        head = max(self.k, n // self.HEAD_FRACTION)
-        return head if head < n else 0
-
-    def _set_floor(self, head: int) -> None:
-        """Floor = k-th best exact score of the head (16-bit results needing the
-        32-bit rescue are left out): a lower bound of the final k-th best."""
-        o = self.out
-        s = o["score"][:head].masked_fill((o["flags"][:head] & _lib.FLAG_RESCUE) != 0, 0)
-        kk = min(self.k, head)
-        o["_floor"].copy_(torch.topk(s, kk, sorted=False).values.min().reshape(1))
+    def _sampled_order(self, n: int) -> tuple[torch.Tensor | None, int]:
+        """Processing order for a launch over n length-sorted jobs in coords='topk'
+        mode: (sample, then the rest in length order), and the sample size.
+        (None, 0) when every target gets coordinates."""
+        if self.coords != "topk" or self.plan16.width != 16:
+            return None, 0
+        cache = getattr(self, "_orders", {})
+        if n not in cache:
+            idx = torch.arange(n, dtype=torch.int32, device="cuda")
+            pick = torch.zeros(n, dtype=torch.bool, device="cuda")
+            pick[n // 8::self.SAMPLE_STRIDE] = True
+            cnt = int(pick.sum().item())
+            if cnt < self.k:
+                cache[n] = (None, 0)
+            else:
+                cache[n] = (torch.cat([idx[pick], idx[~pick]]).contiguous(), cnt)
+            self._orders = cache
+        return cache[n]
 
     def _rescue(self, n: int) -> None:
         L = _lib.load()
@@ -208,19 +219,16 @@ class DatabaseSearch:
                                  sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
                                  _ptr(d.length), _ptr(lst), 0, _ptr(cnt), _ptr(o["score"]),
                                  _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
-                                 None, None, None, st))
+                                 None, None, None, 0, 0, st))
         self.launches += 2
 
     def align(self) -> dict:
         assert self.dev is not None and self.prof is not None, "upload() and set_query() first"
         n = self.dev.n
-        head = self._head(n)
-        if head:
-            self._launch16(0, head, floor=False)
-            self._set_floor(head)
-            self._launch16(head, n, floor=True)
-        else:
-            self._launch16(0, n, floor=False)
+        order, sample = self._sampled_order(n)
+        if sample:
+            self.out["_floor"].zero_()
+        self._launch16(0, n, floor=bool(sample), sample=sample, order=order)
         self._rescue(n)
         return self.out
 
@@ -250,22 +258,17 @@ class DatabaseSearch:
                 ev = torch.cuda.Event()
                 ev.record(copy)
             events.append((a, b, ev))
-        head = self._head(n)
-        floor_set = False
+        first = int(bounds[1]) if len(bounds) > 1 else 0
+        order, sample = self._sampled_order(first)
+        if sample:
+            o["_floor"].zero_()
         for a, b, ev in events:
             cur.wait_event(ev)
             if b <= a:
                 continue
-            if head and not floor_set and a >= head:
-                self._set_floor(head)
-                floor_set = True
-            if head and a < head < b:  # the head boundary splits this chunk
-                self._launch16(a, head, floor=False)
-                self._set_floor(head)
-                floor_set = True
-                self._launch16(head, b, floor=True)
-            else:
-                self._launch16(a, b, floor=floor_set)
+            # the first chunk samples the floor; later chunks read it
+            self._launch16(a, b, floor=bool(sample), sample=sample if a == 0 else 0,
+                           order=order if a == 0 else None)
         self._rescue(n)
         return o
 
