@@ -342,7 +342,9 @@ sw_striped_kernel(const SwArgs a) {
   // alignments scoring >= *coord_floor, so the per-column gate compares against
   // the floor and the thread's own best -- no group reduction per column. A floor
   // of 0 (not yet raised by the sample) keeps the group-wide gate.
-  const bool has_floor = a.coord_floor != nullptr;
+  // (exact scan instances only: the database-search kernels; elsewhere the floor
+  // code would cost registers and every alignment gets its coordinates)
+  const bool has_floor = EXACT && VAR == VAR_SCAN && a.coord_floor != nullptr;
   const int64_t fs_tasks = (has_floor && a.task_ctr) ? min((a.floor_sample + G - 1) / G, n_tasks) : 0;
   constexpr int kCh = 8, kNch = (LMAX + kCh - 1) / kCh;
 
