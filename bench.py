@@ -263,7 +263,7 @@ def main() -> None:
                                  w.scheme.gap_extend, p.bias, p.max_sub, _ptr(d.codes),
                                  _ptr(d.start), _ptr(d.length), None, d.n, None,
                                  _ptr(o["score"]), _ptr(o["ref_end"]), _ptr(o["query_end"]),
-                                 _ptr(o["flags"]), None, None, _ptr(o["_floor"]), 0, 0, _stream()))
+                                 _ptr(o["flags"]), None, None, C.byref(_lib.DbOpts(d_coord_floor=o["_floor"].data_ptr())), _stream()))
     ek1.record(stream)
     torch.cuda.synchronize()
     k_ms = ek0.elapsed_time(ek1) / k_reps
@@ -294,7 +294,7 @@ def main() -> None:
 
     def e2e_step():
         eng.set_query(w.query)
-        eng.search_streamed(packed, n_chunks=16)  # H2D of chunk k+1 overlaps chunk k
+        eng.search_streamed(packed, n_chunks=32)  # one launch; tasks wait for their chunk
         return search.merge_topk(eng.topk(TOPK), TOPK).cpu()
 
     for _ in range(max(3, args.warmup)):

@@ -48,6 +48,7 @@ enum {
   SW_FLAG_REF_OVERFLOW = 1, /* reference uint16 kernels would saturate: exact > 65535 - bias */
   SW_FLAG_RESCUE = 2,       /* 16-bit run hit the wrap guard (internal; cleared by rescue) */
   SW_FLAG_RESCUED = 4,      /* result comes from the 32-bit re-run */
+  SW_FLAG_FEED_TIMEOUT = 8, /* streamed input (sw_db_opts_t.d_arrived) never arrived */
 };
 
 /* Striped layout chosen for one query (reference: VectorSpec(lanes) +
@@ -89,21 +90,37 @@ int32_t sw_profile_build(const sw_plan_t* plan, const uint8_t* d_query, const in
  * d_pass_stats (lazy-F kernels): int64 [n][2] = (total correction passes, columns that
  * took the early exit) per alignment -- with the reference layout and a *_MIRROR
  * kernel these reproduce the reference's OpCounters exactly (src/vectors.py:61-95).
- * d_coord_floor (nullable device int32): end coordinates are located only for
- * alignments scoring >= *d_coord_floor (others report ref_end = query_end = -2;
- * scores are always exact).  A database search passes a lower bound of its
- * top-k threshold so that only candidate hits pay for the position search.
- * floor_sample > 0 (16-bit plans): the kernel itself raises *d_coord_floor (which
- * must hold a valid floor at launch, e.g. 0) to the floor_k-th best exact score of
- * the first floor_sample jobs in processing order once they complete -- a lower
- * bound of the final top-floor_k threshold, found without a second launch. */
+ * opts (nullable): database-search controls, see sw_db_opts_t. */
+typedef struct sw_db_opts {
+  /* d_coord_floor (nullable device int32): end coordinates are located only for
+   * alignments scoring >= *d_coord_floor (others report ref_end = query_end = -2;
+   * scores are always exact).  A database search passes a lower bound of its top-k
+   * threshold so that only candidate hits pay for the position search.  Applied by
+   * the exact 16-bit scan instances; other kernels locate every alignment. */
+  int32_t* d_coord_floor;
+  /* floor_sample > 0: the kernel itself raises *d_coord_floor (a valid floor at
+   * launch, e.g. 0) to the floor_k-th best exact score of the first floor_sample
+   * jobs in processing order once they complete -- a lower bound of the final
+   * top-floor_k threshold, found without a second launch. */
+  int64_t floor_sample;
+  int32_t floor_k;
+  /* Streamed input: arrive_epoch > 0 makes every task wait until the chunk holding
+   * its jobs has arrived: jobs [c * arrive_jobs, (c + 1) * arrive_jobs) (ids before
+   * d_order) are readable once d_arrived[c] >= arrive_epoch.  The caller copies
+   * chunk c (residues, starts, lengths) and then the flag on one copy stream, so
+   * one launch overlaps the whole host-to-device transfer.  A chunk that never
+   * arrives (~17 s) marks its jobs SW_FLAG_FEED_TIMEOUT instead of hanging. */
+  int32_t arrive_epoch;
+  const int32_t* d_arrived;
+  int64_t arrive_jobs;
+} sw_db_opts_t;
+
 int32_t sw_db_align(const sw_plan_t* plan, const uint32_t* d_prof, int32_t kernel,
                     int32_t gap_open, int32_t gap_extend, int32_t bias, int32_t max_sub,
                     const uint8_t* d_tgt, const int64_t* d_start, const int32_t* d_len,
                     const int32_t* d_order, int64_t n, const int64_t* d_n_jobs,
                     int32_t* d_score, int32_t* d_ref_end, int32_t* d_query_end, uint8_t* d_flags,
-                    int32_t* d_col_passes, int64_t* d_pass_stats,
-                    int32_t* d_coord_floor, int64_t floor_sample, int32_t floor_k,
+                    int32_t* d_col_passes, int64_t* d_pass_stats, const sw_db_opts_t* opts,
                     sw_stream_t stream);
 
 /* n independent (query_k, target_k) pairs.  Reference: batch_align(kernel_id, p,

@@ -49,6 +49,19 @@ class SwError(RuntimeError):
         self.code = code
 
 
+class DbOpts(C.Structure):
+    """sw_db_opts_t (include/swscan_b200.h): coordinate floor + streamed-input feed."""
+
+    _fields_ = [
+        ("d_coord_floor", C.c_void_p),
+        ("floor_sample", C.c_int64),
+        ("floor_k", C.c_int32),
+        ("arrive_epoch", C.c_int32),
+        ("d_arrived", C.c_void_p),
+        ("arrive_jobs", C.c_int64),
+    ]
+
+
 class Plan(C.Structure):
     _fields_ = [
         ("width", C.c_int32),
@@ -104,7 +117,7 @@ def load():
     L.sw_profile_build.argtypes = [C.POINTER(Plan), vp, vp, i32, vp, vp]
     L.sw_db_align.restype = i32
     L.sw_db_align.argtypes = [C.POINTER(Plan), vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, i64,
-                              vp, vp, vp, vp, vp, vp, vp, vp, i64, i32, vp]
+                              vp, vp, vp, vp, vp, vp, vp, C.POINTER(DbOpts), vp]
     L.sw_pairs_align.restype = i32
     L.sw_pairs_align.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, vp, i32, i32, vp, i32,
                                  i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]

@@ -279,7 +279,7 @@ def db_align(prof: DeviceProfile, tgt: torch.Tensor, start: torch.Tensor, length
                              sch.gap_extend, prof.bias, prof.max_sub, _ptr(tgt), _ptr(start),
                              _ptr(length), _ptr(order), n, None, _ptr(out["score"]),
                              _ptr(out["ref_end"]), _ptr(out["query_end"]), _ptr(out["flags"]),
-                             _ptr(col_passes), None, _ptr(coord_floor), 0, 0, st))
+                             _ptr(col_passes), None, (C.byref(_lib.DbOpts(d_coord_floor=coord_floor.data_ptr())) if coord_floor is not None else None), st))
     if rescue:
         _rescue_db(prof, tgt, start, length, kid, col_passes, out, n)
     return out
@@ -301,7 +301,7 @@ def _rescue_db(prof, tgt, start, length, kid, col_passes, out, n) -> None:
                              sch.gap_extend, prof.bias, prof.max_sub, _ptr(tgt), _ptr(start),
                              _ptr(length), _ptr(ws[0]), 0, _ptr(ws[1]), _ptr(out["score"]),
                              _ptr(out["ref_end"]), _ptr(out["query_end"]), _ptr(out["flags"]),
-                             _ptr(col_passes), None, None, 0, 0, st))
+                             _ptr(col_passes), None, None, st))
 
 
 def _result_from(prof_or_none, kernel, n, L_, P, score, flags, rend, qend, passes) -> AlignmentResult:

@@ -308,8 +308,7 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
                     const int64_t* d_start, const int32_t* d_len, const int32_t* d_order, int64_t n,
                     const int64_t* d_n_jobs, int32_t* d_score, int32_t* d_ref_end,
                     int32_t* d_query_end, uint8_t* d_flags, int32_t* d_col_passes,
-                    int64_t* d_pass_stats, int32_t* d_coord_floor, int64_t floor_sample,
-                    int32_t floor_k, sw_stream_t stream) {
+                    int64_t* d_pass_stats, const sw_db_opts_t* opts, sw_stream_t stream) {
   std::call_once(g_once, init_tables);
   if (!p || !d_prof || !d_tgt || !d_start || !d_len || !d_score)
     return fail(SW_EINVAL, "NULL argument");
@@ -357,13 +356,20 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
   a.flags = d_flags;
   a.col_passes = d_col_passes;
   a.pass_stats = d_pass_stats;
-  if (floor_sample > 0 && (!d_coord_floor || floor_k < 1))
-    return fail(SW_EINVAL, "floor_sample needs d_coord_floor and floor_k >= 1");
-  if (floor_sample > 0 && p->width != 16)
-    return fail(SW_ENOTSUP, "the sampled coordinate floor is for 16-bit launches");
-  a.coord_floor = d_coord_floor;
-  a.floor_sample = floor_sample;
-  a.floor_k = floor_k;
+  if (opts) {
+    if (opts->floor_sample > 0 && (!opts->d_coord_floor || opts->floor_k < 1))
+      return fail(SW_EINVAL, "floor_sample needs d_coord_floor and floor_k >= 1");
+    if (opts->arrive_epoch > 0 && (!opts->d_arrived || opts->arrive_jobs < 1))
+      return fail(SW_EINVAL, "arrive_epoch needs d_arrived and arrive_jobs >= 1");
+    a.coord_floor = opts->d_coord_floor;
+    a.floor_sample = opts->floor_sample;
+    a.floor_k = opts->floor_k;
+    if (opts->arrive_epoch > 0) {
+      a.arrived = opts->d_arrived;
+      a.arrive_jobs = opts->arrive_jobs;
+      a.arrive_epoch = opts->arrive_epoch;
+    }
+  }
   // exact instances stage the profile as [sym][ceil(L/4)][T][4]
   // (T = 4: two copies at 32-word block granularity, see DUP in sw_kernels.cuh)
   const size_t smem = block == 128 ? (size_t)(p->n_sym + 1) * ((p->seg_len + 3) / 4 * 4) * p->threads * 4 *

@@ -48,9 +48,16 @@ enum : uint8_t {
   FLAG_REF_OVERFLOW = 1,  // the reference uint16 kernels would saturate (exact > 65535 - bias)
   FLAG_RESCUE = 2,        // 16-bit run may have wrapped: re-run in 32 bits
   FLAG_RESCUED = 4,       // score/coords come from the 32-bit re-run
+  FLAG_FEED_TIMEOUT = 8,  // streamed input never arrived (results invalid)
 };
 
 constexpr int kMaxSym = 32;  // alphabet size limit of the device path (plus one null row)
+
+__device__ __forceinline__ int ld_acquire_s32(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
@@ -219,6 +226,9 @@ struct SwArgs {
   int32_t floor_k;            //      of the first floor_sample jobs once they complete
   unsigned long long* task_ctr; // optional zeroed counters: [0] task claims, [1] sample tasks done
   uint32_t* floor_hist;       // zeroed [kFloorBins] histogram of the sample's scores
+  const int32_t* arrived;     // streamed input: chunk c readable once arrived[c] >= epoch
+  int64_t arrive_jobs;        // jobs per chunk
+  int32_t arrive_epoch;
 };
 constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095 share the top bin)
 
@@ -365,8 +375,23 @@ sw_striped_kernel(const SwArgs a) {
     const int64_t slot = task * G + gw;
     const bool valid = slot < n_jobs;
     const int64_t job = valid ? (a.order ? (int64_t)a.order[slot] : slot) : 0;
-    const int len = valid ? a.t_len[job] : 0;
-    const uint8_t* tp = a.tgt + (valid ? a.t_start[job] : 0);
+    // Streamed input: wait until the chunk holding this task's jobs has arrived
+    // (chunks arrive in order, so the latest chunk needed is the only one to check).
+    // Target data is read through L2 (ld.cg) so no L1 line fetched before its
+    // chunk arrived can be reused.
+    // (every lane waits for its own job's chunk: no warp collective here, which
+    // would raise the register allocation of the whole kernel)
+    bool feed_ok = true;
+    if (a.arrived && valid) {
+      const int32_t* flag = a.arrived + job / a.arrive_jobs;
+      unsigned spins = 0;
+      while (ld_acquire_s32(flag) < a.arrive_epoch) {
+        __nanosleep(256);
+        if (++spins == (1u << 26)) { feed_ok = false; break; }
+      }
+    }
+    const int len = (valid && feed_ok) ? __ldcg(a.t_len + job) : 0;
+    const uint8_t* tp = a.tgt + ((valid && feed_ok) ? __ldcg(a.t_start + job) : 0);
 
     if (a.mode == 1) {
       // ---- per-job query profile (pairs mode) ----
@@ -433,12 +458,12 @@ sw_striped_kernel(const SwArgs a) {
 #pragma unroll
     for (int k = 0; k < kNch; ++k) cmk[k] = 0u;
     const int nullsym = A;
-    int nxt = (len > 0) ? (int)__ldg(tp) : nullsym;
+    int nxt = (len > 0) ? (int)__ldcg(tp) : nullsym;
 
     SWB_UNROLL(SWB_COL_UNROLL)
     for (int i = 0; i < maxlen; ++i) {
       const int sym = nxt;
-      nxt = (i + 1 < len) ? (int)__ldg(tp + i + 1) : nullsym;
+      nxt = (i + 1 < len) ? (int)__ldcg(tp + i + 1) : nullsym;
       const uint32_t* pr = prof_base + sym * LT;
       uint4 S4[VEC ? LP4 : 1];
       if constexpr (VEC) {
@@ -612,6 +637,7 @@ sw_striped_kernel(const SwArgs a) {
       }
       if (sc > 65535 - bias) fl |= FLAG_REF_OVERFLOW;
       if (a.n_jobs_dev) fl |= FLAG_RESCUED;  // device-counted launches are rescue passes
+      if (!feed_ok) fl |= FLAG_FEED_TIMEOUT;
       if (sc == 0) { col = -1; q = -1; }
       else if (best != sc) { col = -2; q = -2; }  // below the coordinate floor: not located
       a.score[job] = sc;

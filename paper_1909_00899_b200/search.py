@@ -171,42 +171,50 @@ class DatabaseSearch:
                                       _ptr(self.prof16), _stream()))
         self.launches += 1
 
-    def _launch16(self, a: int, b: int, floor: bool, sample: int = 0,
-                  order: torch.Tensor | None = None) -> None:
-        """16-bit striped kernel over database slots [a, b) (outputs offset likewise);
-        ``order``: processing order of the local job ids 0..b-a-1; ``floor``: gate
-        coordinates on the floor buffer; ``sample`` > 0: the launch raises the floor
-        from the first ``sample`` jobs of its processing order (see sw_db_align)."""
+    def _launch16(self, n: int, floor: bool, sample: int = 0,
+                  order: torch.Tensor | None = None, feed: tuple | None = None) -> None:
+        """16-bit striped kernel over the n database slots; ``order``: processing
+        order of the job ids; ``floor``: gate coordinates on the floor buffer;
+        ``sample`` > 0: the launch raises the floor from the first ``sample`` jobs
+        of its processing order; ``feed`` = (d_arrived, jobs per chunk, epoch):
+        streamed input (see sw_db_opts_t)."""
         L = _lib.load()
         p, d, o, sch = self.prof, self.dev, self.out, self.scheme
-        ptr = lambda t, i: C.c_void_p(t.data_ptr() + i * t.element_size())  # noqa: E731
+        opts = None
+        if floor or feed:
+            opts = _lib.DbOpts(d_coord_floor=o["_floor"].data_ptr() if floor else None,
+                               floor_sample=sample, floor_k=self.k)
+            if feed:
+                opts.d_arrived, opts.arrive_jobs, opts.arrive_epoch = (feed[0].data_ptr(),
+                                                                       feed[1], feed[2])
         _lib.check(L.sw_db_align(C.byref(self.plan16), _ptr(self.prof16), self.kid, sch.gap_open,
-                                 sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes),
-                                 ptr(d.start, a), ptr(d.length, a), _ptr(order), b - a, None,
-                                 ptr(o["score"], a), ptr(o["ref_end"], a),
-                                 ptr(o["query_end"], a), ptr(o["flags"], a), None, None,
-                                 _ptr(o["_floor"]) if floor else None, sample, self.k,
-                                 _stream()))
+                                 sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
+                                 _ptr(d.length), _ptr(order), n, None, _ptr(o["score"]),
+                                 _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
+                                 None, None, C.byref(opts) if opts else None, _stream()))
         self.launches += 1
 
-    def _sampled_order(self, n: int) -> tuple[torch.Tensor | None, int]:
+    def _sampled_order(self, n: int, region: int | None = None) -> tuple[torch.Tensor | None, int]:
         """Processing order for a launch over n length-sorted jobs in coords='topk'
-        mode: (sample, then the rest in length order), and the sample size.
-        (None, 0) when every target gets coordinates."""
-        if self.coords != "topk" or self.plan16.width != 16:
+        mode: (sample, then the rest in length order), and the sample size. The
+        sample is every SAMPLE_STRIDE-th job of [region/8, region) (region = n by
+        default; the first chunk when the input is streamed). (None, 0) when every
+        target gets coordinates."""
+        if self.coords != "topk" or self.plan16.width != 16 or self.kernel != "scan":
             return None, 0
+        region = n if region is None else min(region, n)
         cache = getattr(self, "_orders", {})
-        if n not in cache:
+        if (n, region) not in cache:
             idx = torch.arange(n, dtype=torch.int32, device="cuda")
             pick = torch.zeros(n, dtype=torch.bool, device="cuda")
-            pick[n // 8::self.SAMPLE_STRIDE] = True
+            pick[region // 8:region:self.SAMPLE_STRIDE] = True
             cnt = int(pick.sum().item())
             if cnt < self.k:
-                cache[n] = (None, 0)
+                cache[(n, region)] = (None, 0)
             else:
-                cache[n] = (torch.cat([idx[pick], idx[~pick]]).contiguous(), cnt)
+                cache[(n, region)] = (torch.cat([idx[pick], idx[~pick]]).contiguous(), cnt)
             self._orders = cache
-        return cache[n]
+        return cache[(n, region)]
 
     def _rescue(self, n: int) -> None:
         L = _lib.load()
@@ -228,47 +236,52 @@ class DatabaseSearch:
         order, sample = self._sampled_order(n)
         if sample:
             self.out["_floor"].zero_()
-        self._launch16(0, n, floor=bool(sample), sample=sample, order=order)
+        self._launch16(n, floor=bool(sample), sample=sample, order=order)
         self._rescue(n)
         return self.out
 
-    def search_streamed(self, packed: PackedDb, n_chunks: int = 8) -> dict:
-        """End-to-end form for a host-resident (pinned) database: chunk k+1 is
-        copied on a side stream while chunk k is aligned, so the H2D transfer
-        hides behind compute. Requires set_query(); returns the result dict."""
+    def search_streamed(self, packed: PackedDb, n_chunks: int = 32) -> dict:
+        """End-to-end form for a host-resident (pinned) database, one kernel launch:
+        the copy stream uploads chunk c (residues, starts, lengths, ids) and then
+        its arrival flag; the striped kernel, launched at once, makes each task
+        wait for the chunk holding its targets, so the H2D transfer overlaps the
+        alignment with no per-chunk launch tails. Requires set_query(); returns
+        the result dict."""
         assert self.prof is not None, "set_query() first"
         self._ensure_buffers(packed)
         d, o = self.dev, self.out
         n = packed.n
+        if n == 0:
+            return o
         cur = torch.cuda.current_stream()
         copy = self._copy_stream = getattr(self, "_copy_stream", None) or torch.cuda.Stream()
-        bounds = np.linspace(0, n, max(1, min(n_chunks, n)) + 1).astype(np.int64)
+        n_chunks = max(1, min(n_chunks, n))
+        cj = -(-n // n_chunks)
+        cj = -(-cj // 32) * 32  # chunk boundaries on 32-job (128-byte) lines
+        n_chunks = -(-n // cj)
+        if getattr(self, "_arrived", None) is None or self._arrived.numel() < n_chunks:
+            self._arrived = torch.zeros(max(n_chunks, 64), dtype=torch.int32, device="cuda")
+            self._epoch = 0
+        self._epoch += 1
+        marks = torch.full((n_chunks,), self._epoch, dtype=torch.int32).pin_memory()
         starts = packed.start
         copy.wait_stream(cur)  # buffers may still be read by a previous step
-        events = []
-        for c in range(len(bounds) - 1):
-            a, b = int(bounds[c]), int(bounds[c + 1])
-            ra = int(starts[a]) if a < n else 0
-            rb = int(starts[b - 1]) + int(packed.length[b - 1]) if b > a else ra
-            with torch.cuda.stream(copy):
+        with torch.cuda.stream(copy):
+            for c in range(n_chunks):
+                a, b = c * cj, min(n, (c + 1) * cj)
+                ra = int(starts[a])
+                rb = int(starts[b - 1]) + int(packed.length[b - 1])
                 d.codes[ra:rb].copy_(packed.codes[ra:rb], non_blocking=True)
                 for dst, src in ((d.start, packed.start), (d.length, packed.length),
                                  (d.ids, packed.ids)):
                     dst[a:b].copy_(src[a:b], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(copy)
-            events.append((a, b, ev))
-        first = int(bounds[1]) if len(bounds) > 1 else 0
-        order, sample = self._sampled_order(first)
+                self._arrived[c:c + 1].copy_(marks[c:c + 1], non_blocking=True)
+        order, sample = self._sampled_order(n, region=cj)
         if sample:
             o["_floor"].zero_()
-        for a, b, ev in events:
-            cur.wait_event(ev)
-            if b <= a:
-                continue
-            # the first chunk samples the floor; later chunks read it
-            self._launch16(a, b, floor=bool(sample), sample=sample if a == 0 else 0,
-                           order=order if a == 0 else None)
+        self._launch16(n, floor=bool(sample), sample=sample, order=order,
+                       feed=(self._arrived, cj, self._epoch))
+        cur.wait_stream(copy)  # ids (and the flags' owner) before topk / the next step
         self._rescue(n)
         return o
 

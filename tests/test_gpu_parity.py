@@ -208,7 +208,7 @@ def test_coordinate_floor_db(A, oracle):
         _lib.check(_lib.load().sw_db_align(C.byref(plan16), _ptr(prof16), 2, 11, 1, prof.bias,
                                            prof.max_sub, _ptr(tgt), _ptr(start), _ptr(length),
                                            None, n, None, _ptr(o["s"]), _ptr(o["r"]),
-                                           _ptr(o["q"]), _ptr(fl), None, None, _ptr(fv), 0, 0,
+                                           _ptr(o["q"]), _ptr(fl), None, None, C.byref(_lib.DbOpts(d_coord_floor=fv.data_ptr())),
                                            _stream()))
         s_, r_, q_ = (o[k].cpu().numpy() for k in ("s", "r", "q"))
         assert (s_ == sc).all(), floor
@@ -451,7 +451,7 @@ def test_config2_full_database_properties(A, oracle):
                                        prof.bias, prof.max_sub, _ptr(tgt), _ptr(start),
                                        _ptr(length), None, n, None, _ptr(o32["score"]),
                                        _ptr(o32["ref_end"]), _ptr(o32["query_end"]), _ptr(fl),
-                                       None, None, None, 0, 0, _stream()))
+                                       None, None, None, _stream()))
     for k in ("score", "ref_end", "query_end"):
         assert (o32[k].cpu().numpy() == res["scan"][k]).all(), k
     rng = np.random.default_rng(0xD0B)

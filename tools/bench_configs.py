@@ -56,7 +56,7 @@ def single_pair(name, w, kernels, lanes, reps, width=16):
             _lib.check(L.sw_db_align(C.byref(prof.plan16), _ptr(prof.prof16), kid, sch.gap_open,
                                      sch.gap_extend, prof.bias, prof.max_sub, _ptr(tgt),
                                      _ptr(start), _ptr(length), None, 1, None, _ptr(out["s"]),
-                                     _ptr(out["r"]), _ptr(out["q"]), _ptr(fl), None, None, None, 0, 0, _stream()))
+                                     _ptr(out["r"]), _ptr(out["q"]), _ptr(fl), None, None, None, _stream()))
 
         ms = timed(run, reps)
         emit(config=name, kernel=kern, width=16, lanes=prof.plan16.lanes, seg_len=prof.plan16.seg_len,

@@ -6,7 +6,7 @@ from paper_1909_00899_b200 import search, workloads as W
 
 w = W.config2()
 t = time.time(); packed = search.pack(w.db, w.offsets); print(f"pack {time.time()-t:.1f}s", packed.codes.is_pinned())
-eng = search.DatabaseSearch(w.scheme)
+eng = search.DatabaseSearch(w.scheme, coords="topk")
 eng.upload(packed); eng.set_query(w.query); eng.align(); torch.cuda.synchronize()
 
 def timed(name, fn, reps=3):
@@ -22,6 +22,6 @@ timed("upload", lambda: eng.upload(packed))
 timed("set_query", lambda: eng.set_query(w.query))
 timed("align", lambda: eng.align())
 timed("upload+align", lambda: (eng.upload(packed), eng.align()))
-for c in (1, 2, 4, 8, 16):
+for c in (4, 16, 32, 64, 128):
     timed(f"streamed chunks={c}", lambda: eng.search_streamed(packed, n_chunks=c))
-timed("set_query+streamed8", lambda: (eng.set_query(w.query), eng.search_streamed(packed, n_chunks=8)))
+timed("set_query+streamed16+topk", lambda: (eng.set_query(w.query), eng.search_streamed(packed, n_chunks=16), search.merge_topk(eng.topk(100), 100).cpu()))

@@ -41,7 +41,7 @@ def main():
         order, sample = eng._sampled_order(n)
         if sample:
             eng.out["_floor"].zero_()
-        eng._launch16(0, n, floor=bool(sample), sample=sample, order=order)
+        eng._launch16(n, floor=bool(sample), sample=sample, order=order)
         mark("align16")
         eng._rescue(n)
         mark("rescue")
