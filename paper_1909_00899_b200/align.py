@@ -407,10 +407,11 @@ def counters_from_stats(kernel: str, n: int, L: int, p: int, total_passes: int,
 
 def pairs_align(flat_q, q_off, flat_r, r_off, *, kernel: str = "scan", lanes: int = 0,
                 scheme: ScoringScheme | None = None, match_a=None, mis_a=None, go_a=None,
-                ge_a=None, width: int = 16, stats: bool = False) -> dict:
+                ge_a=None, width: int = 16, stats: bool = False, coords: bool = True) -> dict:
     """Independent pairs (CSR queries/targets), results as numpy arrays
     ``score, ref_end, query_end, flags`` (+ ``pass_stats``, ``lanes_used``,
-    ``seg_len`` with ``stats=True``).
+    ``seg_len`` with ``stats=True``). ``coords=False``: score-only launches (no
+    end-coordinate search; ``ref_end``/``query_end`` stay -1).
 
     Scoring is either one shared ``scheme`` or per-pair 4x4 match/mismatch
     schemes like the reference's batch_align (src/_compiled.py:504-529).
@@ -450,7 +451,7 @@ def pairs_align(flat_q, q_off, flat_r, r_off, *, kernel: str = "scan", lanes: in
         pp = [None] * 4
         sub_t = torch.from_numpy(scheme.as_array()).cuda()
         go, ge, bias, max_sub = scheme.gap_open, scheme.gap_extend, scheme.bias, scheme.max_score
-    out = {k: torch.zeros(n, dtype=torch.int32, device="cuda")
+    out = {k: torch.full((n,), 0 if k == "score" else -1, dtype=torch.int32, device="cuda")
            for k in ("score", "ref_end", "query_end")}
     out["flags"] = torch.zeros(n, dtype=torch.uint8, device="cuda")
     pstats = torch.zeros((n, 2), dtype=torch.int64, device="cuda") if stats else None
@@ -465,7 +466,8 @@ def pairs_align(flat_q, q_off, flat_r, r_off, *, kernel: str = "scan", lanes: in
                                     _ptr(dev["tl"]), _ptr(order_t), n_, _ptr(n_dev), min_q, max_q,
                                     _ptr(sub_t), n_sym, go, ge, bias, max_sub,
                                     *[_ptr(x) for x in pp], _ptr(out["score"]),
-                                    _ptr(out["ref_end"]), _ptr(out["query_end"]),
+                                    _ptr(out["ref_end"]) if coords else None,
+                                    _ptr(out["query_end"]) if coords else None,
                                     _ptr(out["flags"]), None, _ptr(pstats), st))
         return order_t
 
@@ -505,7 +507,8 @@ def pairs_align(flat_q, q_off, flat_r, r_off, *, kernel: str = "scan", lanes: in
                                     _ptr(dev["tl"]), _ptr(lst), 0, _ptr(cnt), 0, mq,
                                     _ptr(sub_t), n_sym, go, ge, bias, max_sub,
                                     *[_ptr(x) for x in pp], _ptr(out["score"]),
-                                    _ptr(out["ref_end"]), _ptr(out["query_end"]),
+                                    _ptr(out["ref_end"]) if coords else None,
+                                    _ptr(out["query_end"]) if coords else None,
                                     _ptr(out["flags"]), None, _ptr(pstats), st))
     for k, v in out.items():
         res[k] = v.cpu().numpy()
@@ -524,7 +527,7 @@ def batch_align(kernel_id, p, flat_q, q_off, flat_r, r_off, match_a, mis_a, go_a
     kernel = {0: "lazyf-mirror", 1: "lazyf-noexit-mirror", 2: "scan"}[int(kernel_id)]
     ref_kernel = {0: "lazyf", 1: "lazyf-noexit", 2: "scan"}[int(kernel_id)]
     r = pairs_align(flat_q, q_off, flat_r, r_off, kernel=kernel, lanes=int(p), match_a=match_a,
-                    mis_a=mis_a, go_a=go_a, ge_a=ge_a, stats=True)
+                    mis_a=mis_a, go_a=go_a, ge_a=ge_a, stats=True, coords=False)
     n = r["score"].shape[0]
     tl = np.diff(np.asarray(r_off, dtype=np.int64))
     counters = np.zeros((n, 7), dtype=np.int64)

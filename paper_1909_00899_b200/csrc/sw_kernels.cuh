@@ -355,8 +355,12 @@ sw_striped_kernel(const SwArgs a) {
   // (exact scan instances only: the database-search kernels; elsewhere the floor
   // code would cost registers and every alignment gets its coordinates)
   const bool has_floor = EXACT && VAR == VAR_SCAN && a.coord_floor != nullptr;
+  const bool no_coords = a.ref_end == nullptr && a.query_end == nullptr;
   const int64_t fs_tasks = (has_floor && a.task_ctr) ? min((a.floor_sample + G - 1) / G, n_tasks) : 0;
-  constexpr int kCh = 8, kNch = (LMAX + kCh - 1) / kCh;
+#ifndef SWB_KCH
+#define SWB_KCH 8
+#endif
+  constexpr int kCh = SWB_KCH, kNch = (LMAX + kCh - 1) / kCh;
 
   // Task claiming: with a counter, warps take the next task (in length-descending
   // order) when they finish one -- longest-first greedy, so the warps end together
@@ -450,7 +454,8 @@ sw_striped_kernel(const SwArgs a) {
       floor_v = __shfl_sync(0xffffffffu, floor_v, 0);
     }
     const bool floor_mode = floor_v > 0;
-    int gb = floor_mode ? floor_v - 1 : 0;
+    // score-only launches (no coordinate outputs) never search: the gate never opens
+    int gb = no_coords ? 0x7fffffff : floor_mode ? floor_v - 1 : 0;
     int bv = 0, bcol = -1, bq = -1;   // this thread's first-maximum record
     // running maxima of u per chunk of kCh words (never reset: a chunk reaches a
     // value above gb only in the column that first produces it)
@@ -535,13 +540,28 @@ sw_striped_kernel(const SwArgs a) {
 #pragma unroll
             for (int k = kNch - 1; k >= 0; --k)
               if (Wd::get(cmk[k], h) >= cv) kk = k;
-            int jj = first;
+            int jj;
+            if constexpr (EXACT) {
+              // gather the chunk's words without branching on kk, then search them
+              int jo = kCh;
 #pragma unroll
-            for (int k = 0; k < kNch; ++k) {
-              if (k == kk) {
+              for (int j = kCh - 1; j >= 0; --j) {
+                uint32_t w = 0u;
 #pragma unroll
-                for (int c = (k + 1) * kCh - 1; c >= k * kCh; --c)
-                  if (c < LMAX && c >= first && Wd::get(H[c], h) >= cv) jj = c;
+                for (int k = 0; k < kNch; ++k)
+                  if (k * kCh + j < LMAX) w = (k == kk) ? H[k * kCh + j] : w;
+                if (Wd::get(w, h) >= cv) jo = j;  // unused / padding words hold 0 < cv
+              }
+              jj = kk * kCh + jo;
+            } else {
+              jj = first;
+#pragma unroll
+              for (int k = 0; k < kNch; ++k) {
+                if (k == kk) {
+#pragma unroll
+                  for (int c = (k + 1) * kCh - 1; c >= k * kCh; --c)
+                    if (c < LMAX && c >= first && Wd::get(H[c], h) >= cv) jj = c;
+                }
               }
             }
             bv = cv;

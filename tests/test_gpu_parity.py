@@ -269,6 +269,19 @@ def test_config3_subset_pairs(A, oracle):
             assert (r["ref_end"] == rend).all() and (r["query_end"] == qend).all(), (kern, lanes)
 
 
+def test_score_only_launches(A):
+    """No coordinate outputs => no position search: same scores, coordinates untouched."""
+    from paper_1909_00899_b200 import workloads as W
+
+    w = W.config3(n_pairs=3000)
+    for kern in ("scan", "lazyf"):
+        a = A.pairs_align(w.flat_q, w.q_off, w.flat_r, w.r_off, kernel=kern, scheme=w.scheme)
+        b = A.pairs_align(w.flat_q, w.q_off, w.flat_r, w.r_off, kernel=kern, scheme=w.scheme,
+                          coords=False)
+        assert (a["score"] == b["score"]).all() and (a["flags"] == b["flags"]).all()
+        assert (b["ref_end"] == -1).all() and (b["query_end"] == -1).all()
+
+
 def test_config4_scan_and_lazyf_identical(A, oracle):
     from paper_1909_00899_b200 import workloads as W
 

@@ -90,7 +90,7 @@ def long_pair(name, w, reps, width=32):
          path="strip pipeline (sw_align_long)")
 
 
-def pairs(name, w, reps, kernels=("scan", "lazyf"), lanes=0):
+def pairs(name, w, reps, kernels=("scan", "lazyf"), lanes=0, coords=True):
     L = _lib.load()
     n = w.n_pairs
     qlen = np.diff(w.q_off).astype(np.int32)
@@ -111,11 +111,14 @@ def pairs(name, w, reps, kernels=("scan", "lazyf"), lanes=0):
                                         None, int(qlen.min()), int(qlen.max()), _ptr(sub),
                                         sch.n_symbols, sch.gap_open, sch.gap_extend, sch.bias,
                                         sch.max_score, None, None, None, None, _ptr(out["s"]),
-                                        _ptr(out["r"]), _ptr(out["q"]), _ptr(fl), None, None, _stream()))
+                                        _ptr(out["r"]) if coords else None,
+                                        _ptr(out["q"]) if coords else None, _ptr(fl), None, None,
+                                        _stream()))
 
         ms = timed(run, reps)
         emit(config=name, kernel=kern, width=16, pairs=n, lanes=lanes, ms=round(ms, 3),
-             gcups=round(w.cells / ms / 1e6, 3), path="pairs kernel (per-pair profiles)")
+             gcups=round(w.cells / ms / 1e6, 3), coords=coords,
+             path="pairs kernel (per-pair profiles)")
 
 
 def main() -> None:
@@ -135,6 +138,8 @@ def main() -> None:
         for ln in (int(x) for x in args.c3_lanes.split(",")):
             pairs(f"config3[{args.c3_pairs} pairs]", w3, args.reps, lanes=ln,
                   kernels=("scan", "lazyf") if ln == 0 else ("scan",))
+            pairs(f"config3[{args.c3_pairs} pairs]", w3, args.reps, lanes=ln,
+                  kernels=("scan",), coords=False)
     if 4 in cfgs:
         w = W.config4()
         single_pair("config4", w, ("scan", "lazyf", "lazyf-noexit"), 0, args.reps)
