@@ -132,7 +132,8 @@ def main() -> None:
     if 1 in cfgs:
         w = W.config1()
         single_pair("config1", w, ("scan", "lazyf", "lazyf-noexit"), 0, args.reps * 10)
-        single_pair("config1", w, ("scan", "lazyf"), 64, args.reps * 10)
+        for ln in (16, 32, 64):
+            single_pair("config1", w, ("scan", "lazyf"), ln, args.reps * 10)
     if 3 in cfgs:
         w3 = W.config3(n_pairs=args.c3_pairs)
         for ln in (int(x) for x in args.c3_lanes.split(",")):
