@@ -324,7 +324,7 @@ def main() -> None:
 
     def e2e_step():
         eng.set_query(w.query)
-        eng.search_streamed(packed, n_chunks=32)  # one launch; tasks wait for their chunk
+        eng.search_streamed(packed, n_chunks=64)  # one launch; tasks wait for their chunk
         return search.merge_topk(eng.topk(TOPK), TOPK).cpu()
 
     for _ in range(max(3, args.warmup)):

@@ -240,7 +240,7 @@ class DatabaseSearch:
         self._rescue(n)
         return self.out
 
-    def search_streamed(self, packed: PackedDb, n_chunks: int = 32) -> dict:
+    def search_streamed(self, packed: PackedDb, n_chunks: int = 64) -> dict:
         """End-to-end form for a host-resident (pinned) database, one kernel launch:
         the copy stream uploads chunk c (residues, starts, lengths, ids) and then
         its arrival flag; the striped kernel, launched at once, makes each task
@@ -263,25 +263,29 @@ class DatabaseSearch:
             self._arrived = torch.zeros(max(n_chunks, 64), dtype=torch.int32, device="cuda")
             self._epoch = 0
         self._epoch += 1
+        key = (id(packed), n, cj)
+        if getattr(self, "_chunk_key", None) != key:  # residue ranges of the chunks
+            st, ln = packed.start.numpy(), packed.length.numpy()
+            self._chunks = [(c * cj, min(n, (c + 1) * cj), int(st[c * cj]),
+                             int(st[min(n, (c + 1) * cj) - 1] + ln[min(n, (c + 1) * cj) - 1]))
+                            for c in range(n_chunks)]
+            self._chunk_key = key
         marks = torch.full((n_chunks,), self._epoch, dtype=torch.int32).pin_memory()
-        starts = packed.start
         copy.wait_stream(cur)  # buffers may still be read by a previous step
-        with torch.cuda.stream(copy):
-            for c in range(n_chunks):
-                a, b = c * cj, min(n, (c + 1) * cj)
-                ra = int(starts[a])
-                rb = int(starts[b - 1]) + int(packed.length[b - 1])
-                d.codes[ra:rb].copy_(packed.codes[ra:rb], non_blocking=True)
-                for dst, src in ((d.start, packed.start), (d.length, packed.length),
-                                 (d.ids, packed.ids)):
-                    dst[a:b].copy_(src[a:b], non_blocking=True)
-                self._arrived[c:c + 1].copy_(marks[c:c + 1], non_blocking=True)
+        # launch first (its tasks wait for their chunk), then feed the chunks
         order, sample = self._sampled_order(n, region=cj)
         if sample:
             o["_floor"].zero_()
         self._launch16(n, floor=bool(sample), sample=sample, order=order,
                        feed=(self._arrived, cj, self._epoch))
-        cur.wait_stream(copy)  # ids (and the flags' owner) before topk / the next step
+        with torch.cuda.stream(copy):
+            for c, (a, b, ra, rb) in enumerate(self._chunks):
+                d.codes[ra:rb].copy_(packed.codes[ra:rb], non_blocking=True)
+                d.start[a:b].copy_(packed.start[a:b], non_blocking=True)
+                d.length[a:b].copy_(packed.length[a:b], non_blocking=True)
+                self._arrived[c:c + 1].copy_(marks[c:c + 1], non_blocking=True)
+            d.ids[:n].copy_(packed.ids, non_blocking=True)  # for top-k only
+        cur.wait_stream(copy)  # ids before topk; the copy stream's work before the next step
         self._rescue(n)
         return o
 
