@@ -367,14 +367,15 @@ def main() -> None:
                        "l2": "inputs 359 MB > 126 MB L2 (no flush)",
                        "parallelism": f"db-shard x{world}", "lanes": eng.plan16.lanes,
                        "seg_len": eng.plan16.seg_len,
-                       "end_coords": "exact for every target scoring >= the k-th best of the "
-                                     "longest 1/16 (a superset of the top-k)"},
+                       "end_coords": "exact for every target scoring >= the in-kernel floor "
+                                     "(k-th best of a strided 1/16 sample: a superset of the "
+                                     "top-k); others score-only"},
             "roofline": {"bound": "dpx", "achieved": round(kernel_gcups, 2),
                          "peak": round(peak_gcups, 2), "unit": "GCUPS",
                          "frac": round(kernel_gcups / peak_gcups, 4),
                          # dram__bytes_read+write per launch of this kernel (one ncu --set
-                         # full capture at this config, profiles/r01_config2_db_kernel.md)
-                         "traffic": 516.44e6,
+                         # full capture at this config, profiles/r01d_config2_db_kernel.md)
+                         "traffic": 509.18e6,
                          "kernel": (f"sw_striped_kernel<W16,T={eng.plan16.threads},"
                                     f"L={eng.plan16.seg_len},{args.kernel.upper()},ge={w.scheme.gap_extend}>"),
                          "kernel_ms": round(k_ms, 3),
