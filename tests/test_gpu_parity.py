@@ -282,6 +282,55 @@ def test_score_only_launches(A):
         assert (b["ref_end"] == -1).all() and (b["query_end"] == -1).all()
 
 
+def test_edge_cases_empty_and_tiny(A, oracle):
+    """Zero-length targets and queries, 1-residue sequences, a query whose every
+    cell scores <= 0: exact scores, (-1, -1) coordinates for score 0, both kernels."""
+    import torch as T
+
+    from paper_1909_00899_b200 import search
+
+    rng = np.random.default_rng(0xED6E)
+    sch = mm(2, -3, 5, 2)
+    lens = np.array([0, 1, 2, 5, 0, 100, 1, 0, 37, 64, 65, 3], dtype=np.int64)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    db = rng.integers(0, 4, int(offs[-1])).astype(np.uint8)
+    for q in (np.array([2], np.uint8), rng.integers(0, 4, 7).astype(np.uint8),
+              rng.integers(0, 4, 150).astype(np.uint8)):
+        sc, re_, qe = oracle.db_scalar(q, db, offs, sch.as_array(), 5, 2)
+        prof = A.build_profile_arrays(q, sch)
+        tgt = T.from_numpy(db).cuda()
+        start = T.from_numpy(offs[:-1].copy()).cuda()
+        length = T.from_numpy(lens.astype(np.int32)).cuda()
+        for kern in ("scan", "lazyf"):
+            out = A.db_align(prof, tgt, start, length, None, kern)
+            assert (out["score"].cpu().numpy() == sc).all(), (kern, len(q))
+            assert (out["ref_end"].cpu().numpy() == re_).all(), (kern, len(q))
+            assert (out["query_end"].cpu().numpy() == qe).all(), (kern, len(q))
+        # the search engine over the same database (streamed, top-k coordinates)
+        eng = search.DatabaseSearch(sch, coords="topk", k=3)
+        eng.set_query(q)
+        o = eng.search_streamed(search.pack(db, offs), n_chunks=4)
+        ids = eng.dev.ids.cpu().numpy()
+        assert (o["score"].cpu().numpy() == sc[ids]).all()
+    # pairs with empty sides
+    ql = np.array([0, 3, 1, 0, 20], np.int64)
+    tl = np.array([4, 0, 1, 0, 30], np.int64)
+    q_off = np.concatenate([[0], np.cumsum(ql)]).astype(np.int64)
+    r_off = np.concatenate([[0], np.cumsum(tl)]).astype(np.int64)
+    fq = rng.integers(0, 4, int(q_off[-1])).astype(np.uint8)
+    fr = rng.integers(0, 4, int(r_off[-1])).astype(np.uint8)
+    s, re_, qe = oracle.batch_scalar(fq, q_off, fr, r_off, sub=sch.as_array(), go=5, ge=2)
+    for kern in ("scan", "lazyf"):
+        got = A.pairs_align(fq, q_off, fr, r_off, kernel=kern, scheme=sch)
+        assert (got["score"] == s).all() and (got["ref_end"] == re_).all()
+        assert (got["query_end"] == qe).all()
+    # a scheme under which nothing scores: every alignment is 0 at (-1, -1)
+    neg = mm(-1, -1, 3, 1)
+    out = A.align_pair("scan", 8, rng.integers(0, 4, 40).astype(np.uint8),
+                       rng.integers(0, 4, 90).astype(np.uint8), neg)
+    assert (out.score, out.ref_end, out.query_end) == (0, -1, -1)
+
+
 def test_config4_scan_and_lazyf_identical(A, oracle):
     from paper_1909_00899_b200 import workloads as W
 
