@@ -41,6 +41,7 @@ enum {
   SW_KERNEL_SCAN = 2,
   SW_KERNEL_LAZYF_MIRROR = 3,
   SW_KERNEL_LAZYF_NOEXIT_MIRROR = 4,
+  SW_KERNEL_WAVEFRONT = 5, /* sw_align_long only: strips with an intra-strip wavefront */
 };
 
 /* per-alignment flag bits */

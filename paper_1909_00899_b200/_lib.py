@@ -21,6 +21,7 @@ KERNEL_IDS = {  # reference _KERNEL_IDS (src/_compiled.py:576) + parity-mode laz
     "scan": 2,
     "lazyf-mirror": 3,
     "lazyf-noexit-mirror": 4,
+    "wavefront": 5,  # sw_align_long only: strip pipeline with an intra-strip wavefront
 }
 FLAG_REF_OVERFLOW, FLAG_RESCUE, FLAG_RESCUED = 1, 2, 4
 

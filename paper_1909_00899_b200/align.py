@@ -235,7 +235,7 @@ def align_long(query, ref, scheme: ScoringScheme, width: int = 32, kernel: str =
     sub = torch.from_numpy(scheme.as_array()).cuda()
     out = torch.zeros(4, dtype=torch.int32, device="cuda")
     fl = torch.zeros(1, dtype=torch.uint8, device="cuda")
-    for w in ((16, 32) if width == 16 else (32,)):
+    for w in ((16, 32) if width == 16 and kernel != "wavefront" else (32,)):
         nbytes = L.sw_long_workspace_bytes(m, n, scheme.n_symbols, w)
         if nbytes < 0:
             _lib.check(int(nbytes))

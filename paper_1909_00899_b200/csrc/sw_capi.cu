@@ -35,6 +35,7 @@ KernelTable g_tab[2][3];
 ExactTable g_exact;  // 16-bit scan, exact segment length
 const void* g_chain[2][6];  // strip pipeline [width][L = 1, 2, 4, 8, 16, 32]
 const void* g_chain_prof[2];
+const void* g_wave[4];  // strip pipeline, intra-strip wavefront [L = 1, 2, 4, 8]
 std::once_flag g_once;
 
 void init_tables() {
@@ -52,6 +53,7 @@ void init_tables() {
   swb_fill_exact_t4_g0_e(g_exact); swb_fill_exact_t4_g1_e(g_exact); swb_fill_exact_t4_g2_e(g_exact);
   swb_fill_exact_t4_g0_f(g_exact); swb_fill_exact_t4_g1_f(g_exact); swb_fill_exact_t4_g2_f(g_exact);
   swb_fill_chain(g_chain, g_chain_prof);
+  swb_fill_wave(g_wave);
   swb_fill_w16_scan(g_tab[0][VAR_SCAN]);
   swb_fill_w16_lazyf(g_tab[0][VAR_LAZYF]);
   swb_fill_w16_mirror(g_tab[0][VAR_LAZYF_MIRROR]);
@@ -518,10 +520,44 @@ static ChainGeo chain_geo(int64_t m, int64_t n, int n_sym, int width) {
   return g;
 }
 
+// Wavefront strips (32-bit): per-step latency (cycles) of one strip alone and in a
+// full pipeline; total ~ (n + 4K * nb) * t(L) (a strip trails the one above by ~4
+// tiles).  Measured with tools/chain_latency.py --kernel wavefront.
+static ChainGeo wave_geo(int64_t m, int64_t n, int n_sym) {
+  static const int Ls[4] = {1, 2, 4, 8};
+  static const double lat_alone[4] = {84, 83, 96, 205};
+  static const double lat_loaded[4] = {226, 166, 138, 260};
+  ChainGeo g{};
+  double best = 1e300;
+  int force = 0;
+  if (const char* f = getenv("SWB_WAVE_L")) force = atoi(f);
+  for (int li = 0; li < 4; ++li) {
+    const int L = Ls[li];
+    const int64_t rows = 32LL * L;
+    const int64_t nb = (m + rows - 1) / rows;
+    const double load = nb >= 518 ? 1.0 : (double)nb / 518.0;
+    const double lat = lat_alone[li] + load * (lat_loaded[li] - lat_alone[li]);
+    double cost = (double)(n + nb * 4 * kChainK) * lat;  // a strip trails by ~4 tiles
+    if (nb > 148 * 16 && li < 3) cost *= 1e6;
+    if (force) cost = (L == force) ? 0.0 : 1e300;
+    if (cost < best) {
+      best = cost;
+      g.li = li; g.L = L; g.nb = (int)(nb < 1 ? 1 : nb);
+    }
+  }
+  g.prof_words = (size_t)g.nb * (n_sym + 1) * g.L * 32;
+  g.ring_bytes = (size_t)g.nb * kChainRing * kChainK * sizeof(int2);
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  g.total = al(g.prof_words * 4) + al(g.ring_bytes) + al(g.nb * 128) * 2 + al(g.nb * 16) + 256;
+  return g;
+}
+
 int64_t sw_long_workspace_bytes(int64_t m, int64_t n, int32_t n_sym, int32_t width) {
   if ((width != 16 && width != 32) || n_sym < 1 || n_sym > kMaxSym || m < 1)
     return fail(SW_EINVAL, "bad long-pair shape");
-  return (int64_t)chain_geo(m, n, n_sym, width).total;
+  // enough for either schedule (scan strips or wavefront strips)
+  const size_t c = chain_geo(m, n, n_sym, width).total, w = wave_geo(m, n, n_sym).total;
+  return (int64_t)(c > w ? c : w);
 }
 
 int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int64_t m,
@@ -533,11 +569,17 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
   std::call_once(g_once, init_tables);
   if (!d_query || !d_ref || !d_sub || !d_workspace || !d_score) return fail(SW_EINVAL, "NULL argument");
   if (width != 16 && width != 32) return fail(SW_EINVAL, "width must be 16 or 32");
-  if (kernel != SW_KERNEL_SCAN) return fail(SW_ENOTSUP, "the strip pipeline runs the scan kernel only");
+  if (kernel != SW_KERNEL_SCAN && kernel != SW_KERNEL_WAVEFRONT)
+    return fail(SW_ENOTSUP, "the strip pipeline runs the scan or wavefront kernel");
+  const bool wave = kernel == SW_KERNEL_WAVEFRONT;
+  if (wave) width = 32;  // the wavefront strips compute in 32-bit lanes
+  if (wave && (m > (1LL << 30) || n > (1LL << 30))) return fail(SW_ENOTSUP, "wavefront: sequences up to 2^30");
+  if (wave && (double)(m < n ? m : n) * (max_sub > 0 ? max_sub : 1) >= (double)(1 << 27))
+    return fail(SW_ENOTSUP, "wavefront: scores must stay below 2^27 (use the scan kernel)");
   if (!(gap_open >= gap_extend && gap_extend >= 1)) return fail(SW_EINVAL, "require gap_open >= gap_extend >= 1");
   if (m < 1 || n < 1) return fail(SW_EINVAL, "empty sequence");
   if (n_sym < 1 || n_sym > kMaxSym) return fail(SW_ENOTSUP, "alphabet size %d", n_sym);
-  const ChainGeo g = chain_geo(m, n, n_sym, width);
+  const ChainGeo g = wave ? wave_geo(m, n, n_sym) : chain_geo(m, n, n_sym, width);
   if ((size_t)workspace_bytes < g.total) return fail(SW_EINVAL, "workspace too small (%zu B needed)", g.total);
   const int wi = width == 16 ? 0 : 1;
   cudaStream_t s = (cudaStream_t)stream;
@@ -547,7 +589,9 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
   ws += al(g.prof_words * 4);
   int2* ring = (int2*)ws;
   ws += al(g.ring_bytes);
-  char* zero_begin = ws;
+  // zeroed per launch: counters, bests, ticket; for the wavefront also the ring (its
+  // entries are validated by a generation tag, which must not match stale data)
+  char* zero_begin = wave ? (char*)ring : ws;
   unsigned long long* published = (unsigned long long*)ws;  // one 128-B line per strip
   ws += al(g.nb * 128);
   unsigned long long* consumed = (unsigned long long*)ws;
@@ -592,8 +636,9 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
     a.trace_tiles = atoi(getenv("SWB_CHAIN_TRACE_TILES"));
     a.reverse = getenv("SWB_CHAIN_REVERSE") != nullptr;
   }
-  const void* fn = g_chain[wi][g.li];
-  const size_t smem = (size_t)(n_sym + 1) * g.L * 32 * 4 + kChainK * (16 + 8);  // + tile staging
+  const void* fn = wave ? g_wave[g.li] : g_chain[wi][g.li];
+  const size_t smem = wave ? (size_t)(n_sym + 1) * g.L * 32 * 4 + 128 + 3 * kChainK * 8  // residues, tile_in, 2 x tile_out
+                           : (size_t)(n_sym + 1) * g.L * 32 * 4 + kChainK * (16 + 8);  // + tile staging
   if (smem > 48 * 1024) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(chain smem)");

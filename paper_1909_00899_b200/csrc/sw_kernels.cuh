@@ -824,3 +824,4 @@ SWB_X_DECL(4, 0, e) SWB_X_DECL(4, 1, e) SWB_X_DECL(4, 2, e)
 SWB_X_DECL(4, 0, f) SWB_X_DECL(4, 1, f) SWB_X_DECL(4, 2, f)
 #undef SWB_X_DECL
 void swb_fill_chain(const void* (&tab)[2][6], const void* (&ptab)[2]);
+void swb_fill_wave(const void* (&tab)[4]);

@@ -409,6 +409,8 @@ def test_long_pair_pipeline_int32_config4(A, oracle):
     for width in (32, 16):
         r = A.align_long(w.query, w.ref, w.scheme, width=width)
         assert (r["score"], r["ref_end"], r["query_end"]) == want, width
+    r = A.align_long(w.query, w.ref, w.scheme, kernel="wavefront")
+    assert (r["score"], r["ref_end"], r["query_end"]) == want
 
 
 def test_long_pair_pipeline_config5_slice(A, oracle):
@@ -419,6 +421,8 @@ def test_long_pair_pipeline_config5_slice(A, oracle):
     want = oracle.scalar(w.query, w.ref, w.scheme.as_array(), 3, 1)
     assert want[0] == int(g["c5slice_scalar"])
     r = A.align_long(w.query, w.ref, w.scheme, width=32)
+    assert (r["score"], r["ref_end"], r["query_end"]) == want
+    r = A.align_long(w.query, w.ref, w.scheme, kernel="wavefront")
     assert (r["score"], r["ref_end"], r["query_end"]) == want
     r = A.align_pair("scan", 0, w.query, w.ref, w.scheme)
     assert (r.score, r.ref_end, r.query_end) == want
@@ -445,6 +449,34 @@ def test_long_pair_pipeline_random(A, oracle):
         for width in (16, 32):
             got = A.align_long(q, r, sch, width=width)
             assert (got["score"], got["ref_end"], got["query_end"]) == want, (trial, width, m, n)
+        got = A.align_long(q, r, sch, kernel="wavefront")
+        assert (got["score"], got["ref_end"], got["query_end"]) == want, (trial, "wave", m, n)
+
+
+@pytest.mark.parametrize("rows_per_lane", [1, 2, 4, 8])
+def test_wavefront_strip_heights(A, oracle, rows_per_lane, monkeypatch):
+    """Every wavefront strip height (forced), ragged last strips, n < 32, planted and
+    random pairs, against the scalar oracle."""
+    from paper_1909_00899_b200.scoring import ScoringScheme
+
+    monkeypatch.setenv("SWB_WAVE_L", str(rows_per_lane))
+    rng = np.random.default_rng(0x3A7E + rows_per_lane)
+    for trial in range(6):
+        k = int(rng.integers(2, 21))
+        mat = rng.integers(-5, 6, (k, k))
+        go = int(rng.integers(1, 12))
+        ge = int(rng.integers(1, go + 1))
+        sch = ScoringScheme.from_array(mat, go, ge)
+        m = int(rng.integers(1, 3000))
+        n = int(rng.integers(1, 1500)) if trial else 17
+        q = rng.integers(0, k, m).astype(np.uint8)
+        r = rng.integers(0, k, n).astype(np.uint8)
+        if trial % 2:
+            blk = q[: min(m, n)]
+            r[: blk.shape[0]] = blk
+        want = oracle.scalar(q, r, mat, go, ge)
+        got = A.align_long(q, r, sch, kernel="wavefront")
+        assert (got["score"], got["ref_end"], got["query_end"]) == want, (trial, m, n)
 
 
 def test_config5_full_size_against_reference_score(A):
@@ -463,6 +495,8 @@ def test_config5_full_size_against_reference_score(A):
     assert sha(w.query, w.ref) == str(g["c5_inputs_sha256"])
     r = A.align_long(w.query, w.ref, w.scheme, width=32)
     assert r["score"] == int(g["c5_scan_p64_score"])
+    rw = A.align_long(w.query, w.ref, w.scheme, kernel="wavefront")
+    assert (rw["score"], rw["ref_end"], rw["query_end"]) == (r["score"], r["ref_end"], r["query_end"])
     assert not g["c5_scan_p64_overflow"]
     # end-coordinate property: the best local alignment ends at (ref_end, query_end),
     # so aligning the prefixes that end there gives the same score, and the cell

@@ -64,7 +64,7 @@ def single_pair(name, w, kernels, lanes, reps, width=16):
              ref_end=int(out["r"].item()), query_end=int(out["q"].item()), path="warp kernel")
 
 
-def long_pair(name, w, reps, width=32):
+def long_pair(name, w, reps, width=32, kernel="scan"):
     L = _lib.load()
     q = torch.from_numpy(w.query).cuda()
     r = torch.from_numpy(w.ref).cuda()
@@ -77,7 +77,8 @@ def long_pair(name, w, reps, width=32):
     sch = w.scheme
 
     def run():
-        _lib.check(L.sw_align_long(width, 2, _ptr(q), m, _ptr(r), n, _ptr(sub), sch.n_symbols,
+        _lib.check(L.sw_align_long(width, _lib.KERNEL_IDS[kernel], _ptr(q), m, _ptr(r), n,
+                                   _ptr(sub), sch.n_symbols,
                                    sch.gap_open, sch.gap_extend, sch.bias, sch.max_score, _ptr(ws),
                                    nbytes, C.c_void_p(out.data_ptr()),
                                    C.c_void_p(out.data_ptr() + 4), C.c_void_p(out.data_ptr() + 8),
@@ -85,9 +86,9 @@ def long_pair(name, w, reps, width=32):
 
     ms = timed(run, reps)
     o = out.cpu().tolist()
-    emit(config=name, kernel="scan", width=width, ms=round(ms, 3),
-         gcups=round(w.cells / ms / 1e6, 3), score=o[0], ref_end=o[1], query_end=o[2],
-         path="strip pipeline (sw_align_long)")
+    emit(config=name, kernel=kernel, width=32 if kernel == "wavefront" else width,
+         ms=round(ms, 3), gcups=round(w.cells / ms / 1e6, 3), score=o[0], ref_end=o[1],
+         query_end=o[2], path="strip pipeline (sw_align_long)")
 
 
 def pairs(name, w, reps, kernels=("scan", "lazyf"), lanes=0, coords=True):
@@ -134,6 +135,7 @@ def main() -> None:
         single_pair("config1", w, ("scan", "lazyf", "lazyf-noexit"), 0, args.reps * 10)
         for ln in (16, 32, 64):
             single_pair("config1", w, ("scan", "lazyf"), ln, args.reps * 10)
+        long_pair("config1", w, args.reps * 10, kernel="wavefront")
     if 3 in cfgs:
         w3 = W.config3(n_pairs=args.c3_pairs)
         for ln in (int(x) for x in args.c3_lanes.split(",")):
@@ -145,8 +147,11 @@ def main() -> None:
         w = W.config4()
         single_pair("config4", w, ("scan", "lazyf", "lazyf-noexit"), 0, args.reps)
         long_pair("config4", w, args.reps, width=32)
+        long_pair("config4", w, args.reps, kernel="wavefront")
     if 5 in cfgs:
-        long_pair("config5", W.config5(), max(1, args.reps // 2), width=32)
+        w5 = W.config5()
+        long_pair("config5", w5, max(1, args.reps // 2), width=32)
+        long_pair("config5", w5, args.reps, kernel="wavefront")
 
 
 if __name__ == "__main__":
