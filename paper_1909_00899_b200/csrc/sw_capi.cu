@@ -589,9 +589,9 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
   ws += al(g.prof_words * 4);
   int2* ring = (int2*)ws;
   ws += al(g.ring_bytes);
-  // zeroed per launch: counters, bests, ticket; for the wavefront also the ring (its
-  // entries are validated by a generation tag, which must not match stale data)
-  char* zero_begin = wave ? (char*)ring : ws;
+  // zeroed per launch: the ring (its entries are validated by a generation tag, which
+  // must not match stale data), counters, bests, ticket
+  char* zero_begin = (char*)ring;
   unsigned long long* published = (unsigned long long*)ws;  // one 128-B line per strip
   ws += al(g.nb * 128);
   unsigned long long* consumed = (unsigned long long*)ws;

@@ -188,6 +188,19 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
 
   int2* ring_in = a.ring + (size_t)(b > 0 ? b - 1 : 0) * RING;
   int2* ring_out = a.ring + (size_t)b * RING;
+  // Handoff without flags or fences (as sw_wave_kernel): one 64-bit word per column
+  // (F_out | tag << 31, H_last), tag = parity of the ring generation, flipped so the
+  // zeroed ring never validates; tiles are loaded one tile ahead and validated when
+  // used; back-pressure polls the consumer's relaxed progress counter only when the
+  // last observed value is insufficient.
+  unsigned long long* ring_out64 = reinterpret_cast<unsigned long long*>(ring_out);
+  const unsigned long long* ring_in64 = reinterpret_cast<const unsigned long long*>(ring_in);
+  auto tag_of = [](int64_t c) -> unsigned { return (((unsigned)(c / RING)) & 1u) ^ 1u; };
+  auto load_raw = [&](int64_t c0) -> unsigned long long {
+    return (c0 + t < n && t < kChainK) ? ld_relaxed(ring_in64 + ((c0 + t) % RING)) : 0ull;
+  };
+  unsigned long long raw_next = b > 0 ? load_raw(0) : 0ull;
+  unsigned long long cons_seen = 0;
 
   for (int64_t t0 = 0; t0 < n; t0 += kChainK) {
     const int kc = (int)min((int64_t)kChainK, n - t0);
@@ -197,22 +210,33 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
     unsigned long long* tr31 = (a.trace && tile < a.trace_tiles && t == T - 1)
                                    ? a.trace + ((size_t)b * a.trace_tiles + tile) * 4 : nullptr;
     if (tr) tr[0] = gtimer();
-    // ---- incoming boundary tile ----
+    // ---- incoming boundary tile (loaded last tile; validate, then load the next) ----
     int fin_l = 0, hl_l = 0;
     if (b > 0) {
-      // every reading lane acquires the producer's release itself
-      wait_ge(a.published + (size_t)(b - 1) * 16, (unsigned long long)(t0 + kc));
-      if (t < kc) {
-        const int2 v = __ldcg(ring_in + ((t0 + t) % RING));
-        fin_l = v.x;
-        hl_l = v.y;
+      const unsigned want = tag_of(t0);
+      const bool mine = t < kc;
+      unsigned long long raw = raw_next;
+      while (!__all_sync(gmask, !mine || (unsigned)((raw >> 31) & 1u) == want)) {
+        if (SWB_CHAIN_SLEEP) __nanosleep(32);
+        raw = load_raw(t0);
       }
-      __syncwarp();
-      if (t == 0) st_release(a.consumed + (size_t)b * 16, (unsigned long long)(t0 + kc));
+      if (mine) {
+        fin_l = (int)((uint32_t)raw & 0x7fffffffu);
+        hl_l = (int)(raw >> 32);
+      }
+      if (t == 0)  // the tile's loads returned (their values are in registers): relaxed
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a.consumed + (size_t)b * 16),
+                     "l"((unsigned long long)(t0 + kc)) : "memory");
+      raw_next = load_raw(t0 + kChainK);
     }
-    // ---- back-pressure before producing this tile (the writing lane acquires) ----
-    if (b + 1 < nb && (SWB_CHAIN_BP_ALL || t == T - 1) && t0 >= RING)
-      wait_ge(a.consumed + (size_t)(b + 1) * 16, (unsigned long long)(t0 - RING + kc));
+    // ---- back-pressure before producing this tile ----
+    if (b + 1 < nb && t0 >= RING) {
+      const unsigned long long need = (unsigned long long)(t0 - RING + kc);
+      if (cons_seen < need) {
+        wait_ge(a.consumed + (size_t)(b + 1) * 16, need);
+        cons_seen = ld_relaxed(a.consumed + (size_t)(b + 1) * 16);
+      }
+    }
     if (tr31) tr31[3] = gtimer();
     __syncwarp();
     if (tr) tr[1] = gtimer();
@@ -308,10 +332,10 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
       if (t == T - 1) tile_out[col_k] = make_int2(Wd::get(fo, Wd::LPW - 1), Wd::get(wnext, Wd::LPW - 1));
     }
     __syncwarp();
-    if (b + 1 < nb) {
-      if (t < kc) ring_out[(t0 + t) % RING] = tile_out[t];
-      __syncwarp();
-      if (t == 0) st_release(a.published + (size_t)b * 16, (unsigned long long)(t0 + kc));
+    if (b + 1 < nb && t < kc) {
+      const int2 e = tile_out[t];
+      __stcg(ring_out64 + ((t0 + t) % RING), ((unsigned long long)(uint32_t)e.y << 32) |
+                                                 (uint32_t)e.x | ((unsigned long long)tag_of(t0) << 31));
     }
     if (tr) tr[2] = gtimer();
   }
