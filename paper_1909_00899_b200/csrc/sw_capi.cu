@@ -488,8 +488,8 @@ static ChainGeo chain_geo(int64_t m, int64_t n, int n_sym, int width) {
   double best = 1e300;
   // measured per-column latency (cycles, 32-bit, B200) of one strip alone and of a
   // strip in a full pipeline (~3.5 strips per SM); tools/chain_latency.py
-  static const double lat_alone[6] = {315, 322, 355, 402, 474, 670};
-  static const double lat_loaded[6] = {506, 485, 501, 533, 624, 822};
+  static const double lat_alone[6] = {315, 323, 356, 404, 486, 670};
+  static const double lat_loaded[6] = {380, 366, 386, 431, 511, 700};
   for (int li = 0; li < 6; ++li) {
     const int L = Ls[li];
     const int64_t rows = 32LL * lpw * L;
@@ -498,7 +498,7 @@ static ChainGeo chain_geo(int64_t m, int64_t n, int n_sym, int width) {
     const double lat = lat_alone[li] + load * (lat_loaded[li] - lat_alone[li]);
     // every strip must be co-resident (cooperative launch): keep well inside
     // 148 SMs x 16 one-warp CTAs unless no strip height fits
-    double cost = (double)(n + nb * kChainK) * lat;
+    double cost = (double)(n + nb * 2 * kChainK) * lat;  // a strip trails by ~2 tiles
     if (nb > 148 * 16 && li < 5) cost *= 1e6;
     if (cost < best) {
       best = cost;
