@@ -574,8 +574,8 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
   const bool wave = kernel == SW_KERNEL_WAVEFRONT;
   if (wave) width = 32;  // the wavefront strips compute in 32-bit lanes
   if (wave && (m > (1LL << 30) || n > (1LL << 30))) return fail(SW_ENOTSUP, "wavefront: sequences up to 2^30");
-  if (wave && (double)(m < n ? m : n) * (max_sub > 0 ? max_sub : 1) >= (double)(1 << 27))
-    return fail(SW_ENOTSUP, "wavefront: scores must stay below 2^27 (use the scan kernel)");
+  if (wave && (double)(m < n ? m : n) * (max_sub > 0 ? max_sub : 1) >= (double)(1 << 23))
+    return fail(SW_ENOTSUP, "wavefront: scores must stay below 2^23 (use the scan kernel)");
   if (!(gap_open >= gap_extend && gap_extend >= 1)) return fail(SW_EINVAL, "require gap_open >= gap_extend >= 1");
   if (m < 1 || n < 1) return fail(SW_EINVAL, "empty sequence");
   if (n_sym < 1 || n_sym > kMaxSym) return fail(SW_ENOTSUP, "alphabet size %d", n_sym);

@@ -34,11 +34,14 @@ __device__ __forceinline__ void wait_ge_tight(const unsigned long long* p, unsig
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
+__host__ __device__ constexpr int wave_lp(int L) { return L <= 1 ? 1 : L <= 2 ? 2 : L <= 4 ? 4 : 8; }
+
 template <int L>
 struct WaveLane {
   uint32_t H[L], E[L], Sn[L];
   uint32_t h_bot, f_bot, hab_prev;
-  int bkey, thr, bcol;  // first-maximum record: key (value * LP + LP - 1 - row), column
+  int tkey;             // this step tile's best key (see wave_step)
+  int bkey, thr, bcol;  // first-maximum record: key, column
 };
 
 template <int L, bool CHECKED>
@@ -92,19 +95,16 @@ __device__ __forceinline__ void wave_step(WaveLane<L>& w, const int s, const int
   }
   w.h_bot = w.H[L - 1];
   w.f_bot = F;
-  // first maximum of this lane (a best cell is a diagonal cell, observed as u): one
-  // max over keys u * LP + (LP - 1 - j), so the largest key holds the largest value
-  // at its first row; a column records only a strictly larger value (key > thr,
-  // thr = best key | (LP - 1)).  Pad rows score the null residue and columns outside
-  // [0, n) see only E values below an earlier u, so neither can record.
-  constexpr int LP = L <= 1 ? 1 : L <= 2 ? 2 : L <= 4 ? 4 : 8;
-  int kmax = 0;
+  // first maximum of this lane (a best cell is a diagonal cell, observed as u): the
+  // step tile keeps one max over keys u * 32LP + (31 - k) * LP + (LP - 1 - j), so the
+  // largest key holds the tile's largest value at its first step (column) and first
+  // row; wave_tile_record folds it in at the tile end.  Pad rows score the null
+  // residue and columns outside [0, n) see only E values below an earlier u, so
+  // neither can hold a first maximum.
+  constexpr int LP = wave_lp(L);
 #pragma unroll
-  for (int j = 0; j < L; ++j) kmax = max(kmax, (int)um[j] * LP + (LP - 1 - j));
-  const bool upd = kmax > w.thr;
-  w.bkey = upd ? kmax : w.bkey;
-  w.thr = upd ? (kmax | (LP - 1)) : w.thr;
-  w.bcol = upd ? i : w.bcol;
+  for (int j = 0; j < L; ++j)
+    w.tkey = max(w.tkey, (int)um[j] * (32 * LP) + ((31 - k) * LP + (LP - 1 - j)));
   // lane 31 parks column i = s - 31 for strip b+1: steps k < 31 finish column tile
   // t0/32 - 1 (tlo), step 31 starts column tile t0/32 (thi)
   if (handoff && lane == 31 && (!CHECKED || (i >= 0 && i < n)))
@@ -153,8 +153,19 @@ __global__ void __launch_bounds__(32) sw_wave_kernel(const ChainArgs a) {
 #pragma unroll
   for (int j = 0; j < L; ++j) { w.H[j] = 0u; w.E[j] = 0u; }
   w.h_bot = w.f_bot = w.hab_prev = 0u;
-  constexpr int LP = L <= 1 ? 1 : L <= 2 ? 2 : L <= 4 ? 4 : 8;
-  w.bkey = 0; w.thr = LP - 1; w.bcol = -1;
+  constexpr int LP = wave_lp(L);
+  constexpr int KB = 32 * LP;  // key units per score point
+  w.bkey = 0; w.thr = KB - 1; w.bcol = -1; w.tkey = 0;
+  // a tile's best key beats the record only with a strictly larger value
+  // (thr = record key | (KB - 1)); its column is t0 + (31 - step) - lane
+  auto tile_record = [&](int t0) {
+    if (w.tkey > w.thr) {
+      w.bkey = w.tkey;
+      w.thr = w.tkey | (KB - 1);
+      w.bcol = t0 + (31 - ((w.tkey / LP) & 31)) - lane;
+    }
+    w.tkey = 0;
+  };
   const int qbase = b * 32 * L + lane * L;
   const int nreal = max(0, min(L, a.m - qbase));  // rows < m
 
@@ -253,6 +264,7 @@ __global__ void __launch_bounds__(32) sw_wave_kernel(const ChainArgs a) {
           wave_step<L, true>(w, t0 + k, k, lane, n, A, nreal, qbase, sref, sprof, tile_in, tlo,
                              thi, handoff, NGO, NGE);
     }
+    tile_record(t0);
   }
   // the last (partial) outgoing tiles
   if (handoff) {
@@ -260,8 +272,8 @@ __global__ void __launch_bounds__(32) sw_wave_kernel(const ChainArgs a) {
     for (int c0 = (tend >= 64 ? tend - 64 : 0); c0 < n; c0 += 32)
       store_tile(c0, min(K, n - c0), tile_out + ((c0 >> 5) & 1) * K);
   }
-  const int bv = w.bkey / LP;
-  int bcol = w.bcol, bq = bv > 0 ? qbase + (LP - 1 - (w.bkey & (LP - 1))) : -1;
+  const int bv = w.bkey / KB;
+  int bcol = bv > 0 ? w.bcol : -1, bq = bv > 0 ? qbase + (LP - 1 - (w.bkey & (LP - 1))) : -1;
   const uint32_t full = 0xffffffffu;
 
   // ---- per-strip best, then the last strip to finish reduces ----
