@@ -46,8 +46,7 @@ struct WaveLane {
 
 template <int L, bool CHECKED>
 __device__ __forceinline__ void wave_step(WaveLane<L>& w, const int s, const int k, const int lane,
-                                          const int n, const int A, const int nreal,
-                                          const int qbase, const uint8_t* sref,
+                                          const int n, const int A, const uint8_t* sref,
                                           const uint32_t* sprof, const int2* tile_in,
                                           int2* tlo, int2* thi, const bool handoff,
                                           const uint32_t NGO, const uint32_t NGE) {
@@ -98,7 +97,7 @@ __device__ __forceinline__ void wave_step(WaveLane<L>& w, const int s, const int
   // first maximum of this lane (a best cell is a diagonal cell, observed as u): the
   // step tile keeps one max over keys u * 32LP + (31 - k) * LP + (LP - 1 - j), so the
   // largest key holds the tile's largest value at its first step (column) and first
-  // row; wave_tile_record folds it in at the tile end.  Pad rows score the null
+  // row; tile_record folds it in at the tile end.  Pad rows score the null
   // residue and columns outside [0, n) see only E values below an earlier u, so
   // neither can hold a first maximum.
   constexpr int LP = wave_lp(L);
@@ -167,7 +166,6 @@ __global__ void __launch_bounds__(32) sw_wave_kernel(const ChainArgs a) {
     w.tkey = 0;
   };
   const int qbase = b * 32 * L + lane * L;
-  const int nreal = max(0, min(L, a.m - qbase));  // rows < m
 
   int2* ring_in = a.ring + (size_t)(b > 0 ? b - 1 : 0) * RING;
   int2* ring_out = a.ring + (size_t)b * RING;
@@ -255,13 +253,13 @@ __global__ void __launch_bounds__(32) sw_wave_kernel(const ChainArgs a) {
     if (interior) {
 #pragma unroll
       for (int k = 0; k < 32; ++k)
-        wave_step<L, false>(w, t0 + k, k, lane, n, A, nreal, qbase, sref, sprof, tile_in, tlo,
+        wave_step<L, false>(w, t0 + k, k, lane, n, A, sref, sprof, tile_in, tlo,
                             thi, handoff, NGO, NGE);
     } else {
 #pragma unroll
       for (int k = 0; k < 32; ++k)
         if (t0 + k < steps)
-          wave_step<L, true>(w, t0 + k, k, lane, n, A, nreal, qbase, sref, sprof, tile_in, tlo,
+          wave_step<L, true>(w, t0 + k, k, lane, n, A, sref, sprof, tile_in, tlo,
                              thi, handoff, NGO, NGE);
     }
     tile_record(t0);
