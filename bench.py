@@ -158,6 +158,17 @@ def cpu_baseline(w, seconds: float) -> dict:
                       f"OpenMP {threads} threads)"}
 
 
+def arm_config(w, args, world: int) -> dict:
+    """The workload description both arms report (the reference arm times a bounded
+    sample of the same workload; the sample is described in its cpu_baseline)."""
+    return {"workload": "config2-protein-db", "query_len": int(w.query.shape[0]),
+            "n_targets": args.n_targets, "residues": int(w.offsets[-1]),
+            "cells": int(w.query.shape[0]) * int(w.offsets[-1]), "kernel": args.kernel,
+            "top_k": TOPK, "matrix": "synthetic-stand-in (BLOSUM62 not in container)",
+            "gaps": "open 11, extend 1 (reference convention)",
+            "l2": "inputs 359 MB > 126 MB L2 (no flush)", "parallelism": f"db-shard x{world}"}
+
+
 def run_reference(args) -> None:
     world, rank, _ = dist_env()
     if rank != 0:
@@ -197,8 +208,7 @@ def run_reference(args) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": "config2-protein-db (bounded sample per step)", "query_len": 464,
-                   "n_targets": args.n_targets, "matrix": "synthetic-stand-in"},
+        "config": arm_config(w, args, world),
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -359,13 +369,7 @@ def main() -> None:
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "s16x2",
             "data": "synthetic",
-            "config": {"workload": "config2-protein-db", "query_len": m,
-                       "n_targets": args.n_targets, "residues": int(w.offsets[-1]),
-                       "cells": total_cells, "kernel": args.kernel, "top_k": TOPK,
-                       "matrix": "synthetic-stand-in (BLOSUM62 not in container)",
-                       "gaps": "open 11, extend 1 (reference convention)",
-                       "l2": "inputs 359 MB > 126 MB L2 (no flush)",
-                       "parallelism": f"db-shard x{world}", "lanes": eng.plan16.lanes,
+            "config": {**arm_config(w, args, world), "lanes": eng.plan16.lanes,
                        "seg_len": eng.plan16.seg_len,
                        "end_coords": "exact for every target scoring >= the in-kernel floor "
                                      "(k-th best of a strided 1/16 sample: a superset of the "
