@@ -133,8 +133,35 @@ def load():
     L.sw_align_long.restype = i32
     L.sw_align_long.argtypes = [i32, i32, vp, i64, vp, i64, vp, i32, i32, i32, i32, i32, vp, i64,
                                 vp, vp, vp, vp, vp]
-    _lib = L
-    return L
+    _lib = _Strict(L)
+    return _lib
+
+
+class _Strict:
+    """The loaded library with arity-checked entry points: ctypes passes surplus
+    arguments of a function with argtypes through as varargs, which for this C ABI
+    would silently shift the stream argument; here a wrong argument count raises."""
+
+    def __init__(self, lib):
+        self._lib = lib
+        for name in EXPORTS:
+            fn = getattr(lib, name)
+            setattr(self, name, self._wrap(name, fn))
+
+    @staticmethod
+    def _wrap(name, fn):
+        n = len(fn.argtypes)
+
+        def call(*args):
+            if len(args) != n:
+                raise TypeError(f"{name}() takes {n} arguments ({len(args)} given)")
+            return fn(*args)
+
+        call.__name__ = name
+        return call
+
+    def __getattr__(self, name):
+        return getattr(self._lib, name)
 
 
 def check(rc: int) -> None:

@@ -148,6 +148,7 @@ class DeviceProfile:
     requested_lanes: int = 0
     plan32: _lib.Plan | None = None
     prof32: torch.Tensor | None = None
+    long32: bool = False  # no 32-bit warp-kernel plan: rescues use the strip pipeline
     extra: dict = field(default_factory=dict)
 
     @property
@@ -175,13 +176,20 @@ class DeviceProfile:
         return self.extra["short"]
 
     def ensure32(self) -> None:
-        if self.plan32 is not None:
+        """Build the 32-bit profile used by overflow rescues. A query longer than the
+        32-bit warp kernels hold (1,024 residues) has none: its rare rescues run
+        through the 32-bit strip pipeline instead (rescue_long)."""
+        if self.plan32 is not None or self.long32:
             return
         lanes = self.requested_lanes if self.requested_lanes and self.requested_lanes <= 32 else 0
         try:
             self.plan32 = _lib.plan_query(self.m, self.scheme.n_symbols, 32, lanes)
         except _lib.SwError:
-            self.plan32 = _lib.plan_query(self.m, self.scheme.n_symbols, 32, 0)  # may raise
+            try:
+                self.plan32 = _lib.plan_query(self.m, self.scheme.n_symbols, 32, 0)
+            except _lib.SwError:
+                self.long32 = True
+                return
         self.prof32 = torch.empty(self.plan32.prof_words, dtype=torch.int32, device="cuda")
         _lib.check(_lib.load().sw_profile_build(C.byref(self.plan32), _ptr(self.query),
                                                  _ptr(self.sub), self.bias, _ptr(self.prof32),
@@ -293,15 +301,35 @@ def _rescue_db(prof, tgt, start, length, kid, col_passes, out, n) -> None:
               torch.zeros(1, dtype=torch.int64, device="cuda"))
         out["_rescue"] = ws
     st = _stream()
+    prof.ensure32()
+    if prof.long32:
+        rescue_long(prof, tgt, start, length, out, n)
+        return
     _lib.check(L.sw_collect_flagged(_ptr(out["flags"]), n, _lib.FLAG_RESCUE, _ptr(ws[0]),
                                     _ptr(ws[1]), st))
-    prof.ensure32()
     sch = prof.scheme
     _lib.check(L.sw_db_align(C.byref(prof.plan32), _ptr(prof.prof32), kid, sch.gap_open,
                              sch.gap_extend, prof.bias, prof.max_sub, _ptr(tgt), _ptr(start),
                              _ptr(length), _ptr(ws[0]), 0, _ptr(ws[1]), _ptr(out["score"]),
                              _ptr(out["ref_end"]), _ptr(out["query_end"]), _ptr(out["flags"]),
                              _ptr(col_passes), None, None, st))
+
+
+def rescue_long(prof, tgt, start, length, out, n) -> None:
+    """Exact 32-bit re-run of the 16-bit wrap-guard hits of a query too long for the
+    32-bit warp kernels: each flagged target goes through the 32-bit scan strip
+    pipeline (sw_align_long). Reads the flags on the host (these are rare: the
+    alignment score must approach 32,767)."""
+    fl = out["flags"][:n]
+    hits = torch.nonzero((fl & _lib.FLAG_RESCUE) != 0).flatten().tolist()
+    for j in hits:
+        s0, ln = int(start[j]), int(length[j])
+        r = align_long(None, None, prof.scheme, width=32, query_dev=prof.query,
+                       ref_dev=tgt[s0:s0 + ln])
+        out["score"][j] = r["score"]
+        out["ref_end"][j] = r["ref_end"]
+        out["query_end"][j] = r["query_end"]
+        out["flags"][j] = (r["flags"] & _lib.FLAG_REF_OVERFLOW) | _lib.FLAG_RESCUED
 
 
 def _result_from(prof_or_none, kernel, n, L_, P, score, flags, rend, qend, passes) -> AlignmentResult:

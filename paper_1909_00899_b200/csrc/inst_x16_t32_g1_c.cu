@@ -1,0 +1,6 @@
+#define SWB_X_T 32
+#define SWB_X_GE 1
+#define SWB_X_LO 33
+#define SWB_X_HI 64
+#define SWB_X_FILL swb_fill_exact_t32_g1_c
+#include "sw_inst_exact.inc"

@@ -46,6 +46,9 @@ void init_tables() {
   swb_fill_exact_t8_g2_a(g_exact); swb_fill_exact_t8_g2_b(g_exact);
   swb_fill_exact_t16_g0_b(g_exact); swb_fill_exact_t16_g1_b(g_exact); swb_fill_exact_t16_g2_b(g_exact);
   swb_fill_exact_t32_g0_b(g_exact); swb_fill_exact_t32_g1_b(g_exact); swb_fill_exact_t32_g2_b(g_exact);
+  // 33..64 words at 32/64 stripes: database queries up to 4,096 residues
+  swb_fill_exact_t16_g0_c(g_exact); swb_fill_exact_t16_g1_c(g_exact); swb_fill_exact_t16_g2_c(g_exact);
+  swb_fill_exact_t32_g0_c(g_exact); swb_fill_exact_t32_g1_c(g_exact); swb_fill_exact_t32_g2_c(g_exact);
   swb_fill_exact_t4_g0_b(g_exact); swb_fill_exact_t4_g1_b(g_exact); swb_fill_exact_t4_g2_b(g_exact);
   swb_fill_exact_t4_g0_a(g_exact); swb_fill_exact_t4_g1_a(g_exact); swb_fill_exact_t4_g2_a(g_exact);
   swb_fill_exact_t4_g0_c(g_exact); swb_fill_exact_t4_g1_c(g_exact); swb_fill_exact_t4_g2_c(g_exact);

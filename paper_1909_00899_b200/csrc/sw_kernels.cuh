@@ -822,6 +822,8 @@ SWB_X_DECL(4, 0, c) SWB_X_DECL(4, 1, c) SWB_X_DECL(4, 2, c)
 SWB_X_DECL(4, 0, d) SWB_X_DECL(4, 1, d) SWB_X_DECL(4, 2, d)
 SWB_X_DECL(4, 0, e) SWB_X_DECL(4, 1, e) SWB_X_DECL(4, 2, e)
 SWB_X_DECL(4, 0, f) SWB_X_DECL(4, 1, f) SWB_X_DECL(4, 2, f)
+SWB_X_DECL(16, 0, c) SWB_X_DECL(16, 1, c) SWB_X_DECL(16, 2, c)
+SWB_X_DECL(32, 0, c) SWB_X_DECL(32, 1, c) SWB_X_DECL(32, 2, c)
 #undef SWB_X_DECL
 void swb_fill_chain(const void* (&tab)[2][6], const void* (&ptab)[2]);
 void swb_fill_wave(const void* (&tab)[4]);

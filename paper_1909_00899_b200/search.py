@@ -29,7 +29,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .align import DeviceProfile, _ptr, _stream, build_profile_arrays
+from .align import DeviceProfile, _ptr, _stream, build_profile_arrays, rescue_long
 from .scoring import ScoringScheme
 
 RECORD_FIELDS = ("score", "target_id", "ref_end", "query_end")
@@ -219,6 +219,9 @@ class DatabaseSearch:
     def _rescue(self, n: int) -> None:
         L = _lib.load()
         p, d, o, sch = self.prof, self.dev, self.out, self.scheme
+        if p.long32:  # query beyond the 32-bit warp kernels: strip-pipeline rescues
+            rescue_long(p, d.codes, d.start, d.length, o, n)
+            return
         st = _stream()
         lst, cnt = o["_rescue"]
         _lib.check(L.sw_collect_flagged(_ptr(o["flags"]), n, _lib.FLAG_RESCUE, _ptr(lst),
@@ -227,7 +230,7 @@ class DatabaseSearch:
                                  sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
                                  _ptr(d.length), _ptr(lst), 0, _ptr(cnt), _ptr(o["score"]),
                                  _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
-                                 None, None, None, 0, 0, st))
+                                 None, None, None, st))
         self.launches += 2
 
     def align(self) -> dict:

@@ -331,6 +331,64 @@ def test_edge_cases_empty_and_tiny(A, oracle):
     assert (out.score, out.ref_end, out.query_end) == (0, -1, -1)
 
 
+@pytest.mark.parametrize("m", [2049, 3000, 4096])
+def test_long_queries_database(A, oracle, m):
+    """Database search with queries of 2,049..4,096 residues (exact 33..64-word
+    segments at 64 stripes) against the scalar oracle, scores and coordinates."""
+    import torch as T
+
+    from paper_1909_00899_b200 import workloads as W
+
+    w = W.config2(n_targets=64)
+    rng = np.random.default_rng(m)
+    q = rng.integers(0, 20, m).astype(np.uint8)
+    q[100:400] = w.db[w.offsets[3]:w.offsets[3] + 300][:300] if w.offsets[4] - w.offsets[3] >= 300 else q[100:400]
+    sc, rend, qend = oracle.db_scalar(q, w.db, w.offsets, w.scheme.as_array(), 11, 1)
+    prof = A.build_profile_arrays(q, w.scheme)
+    assert prof.plan16.seg_len > 32
+    tgt = T.from_numpy(w.db).cuda()
+    start = T.from_numpy(w.offsets[:-1].copy()).cuda()
+    length = T.from_numpy(np.diff(w.offsets).astype(np.int32)).cuda()
+    out = A.db_align(prof, tgt, start, length, None, "scan")
+    assert (out["score"].cpu().numpy() == sc).all()
+    assert (out["ref_end"].cpu().numpy() == rend).all()
+    assert (out["query_end"].cpu().numpy() == qend).all()
+
+
+def test_long_query_database_overflow_rescue(A, oracle):
+    """A 3,500-residue query whose best alignment passes the 16-bit guard: no 32-bit
+    warp-kernel plan exists at that length, so the rescue runs through the 32-bit
+    strip pipeline; the search still returns the exact score and coordinates."""
+    from paper_1909_00899_b200 import search, workloads as W
+
+    w = W.config2(n_targets=40)
+    mat = w.scheme.as_array()
+    top = int(np.argmax(np.diag(mat)))  # the stand-in's W: the largest self score
+    rng = np.random.default_rng(0x3500)
+    q = rng.integers(0, 20, 3500).astype(np.uint8)
+    q[200:3300] = top
+    lens = np.diff(w.offsets)
+    db = w.db.copy()
+    # target 5 holds a 3,100-residue W run: 3,100 * S(W,W) > 32,767
+    t5 = np.full(3100, top, np.uint8)
+    db = np.concatenate([db[: w.offsets[5]], t5, db[w.offsets[6]:]])
+    lens = lens.copy()
+    lens[5] = 3100
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    sc, rend, qend = oracle.db_scalar(q, db, offs, mat, 11, 1)
+    assert sc[5] > 32767
+    eng = search.DatabaseSearch(w.scheme, coords="all")
+    eng.upload(search.pack(db, offs, pin=False))
+    eng.set_query(q)
+    assert eng.prof.long32
+    o = eng.align()
+    ids = eng.dev.ids.cpu().numpy()
+    assert (o["score"].cpu().numpy() == sc[ids]).all()
+    assert (o["ref_end"].cpu().numpy() == rend[ids]).all()
+    assert (o["query_end"].cpu().numpy() == qend[ids]).all()
+    assert (o["flags"].cpu().numpy()[ids == 5] & 4).all()  # rescued
+
+
 def test_config4_scan_and_lazyf_identical(A, oracle):
     from paper_1909_00899_b200 import workloads as W
 

@@ -145,7 +145,7 @@ def main() -> None:
                   kernels=("scan",), coords=False)
     if 4 in cfgs:
         w = W.config4()
-        single_pair("config4", w, ("scan", "lazyf", "lazyf-noexit"), 0, args.reps)
+        single_pair("config4", w, ("scan", "lazyf", "lazyf-noexit"), 64, args.reps)
         long_pair("config4", w, args.reps, width=32)
         long_pair("config4", w, args.reps, kernel="wavefront")
     if 5 in cfgs:
