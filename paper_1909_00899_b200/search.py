@@ -63,6 +63,52 @@ def shard(offsets: np.ndarray, rank: int, world: int) -> np.ndarray:
     return np.sort(by_len[rank::world])
 
 
+def shard_pairs(n_pairs: int, rank: int, world: int) -> tuple[int, int]:
+    """Pair batch sharding (config 3): rank r owns the contiguous range
+    [a, b) of the pairs; pairs are independent, so no exchange is needed."""
+    a = n_pairs * rank // world
+    b = n_pairs * (rank + 1) // world
+    return a, b
+
+
+PACKED_FILES = ("codes", "start", "length", "order", "ids")
+
+
+def save_packed(path: str, packed: PackedDb, alphabet: str | None = None) -> None:
+    """Write a PackedDb as a directory of .npy arrays (memory-mappable) plus meta.json."""
+    import json
+    import os
+
+    os.makedirs(path, exist_ok=True)
+    for name in PACKED_FILES:
+        np.save(os.path.join(path, name + ".npy"), getattr(packed, name).numpy())
+    meta = {"format": "b200-swscan-packed-db", "version": 1, "n": packed.n,
+            "residues": packed.residues, "alphabet": alphabet}
+    with open(os.path.join(path, "meta.json"), "w") as fh:
+        json.dump(meta, fh)
+
+
+def load_packed(path: str, pin: bool = True) -> tuple[PackedDb, dict]:
+    """Read a directory written by save_packed (arrays land in pinned host memory)."""
+    import json
+    import os
+
+    with open(os.path.join(path, "meta.json")) as fh:
+        meta = json.load(fh)
+    if meta.get("format") != "b200-swscan-packed-db":
+        raise ValueError(f"{path}: not a packed database")
+
+    def t(name):
+        a = np.load(os.path.join(path, name + ".npy"), mmap_mode="r")
+        x = torch.from_numpy(np.ascontiguousarray(a))
+        return x.pin_memory() if pin and torch.cuda.is_available() else x
+
+    packed = PackedDb(*(t(name) for name in PACKED_FILES))
+    if packed.n != meta["n"]:
+        raise ValueError(f"{path}: {packed.n} targets, meta says {meta['n']}")
+    return packed, meta
+
+
 def pack(db: np.ndarray, offsets: np.ndarray, ids: np.ndarray | None = None,
          pin: bool = True) -> PackedDb:
     """Pack the targets `ids` (default: all) of a CSR database into a PackedDb,
@@ -243,7 +289,8 @@ class DatabaseSearch:
         self._rescue(n)
         return self.out
 
-    def search_streamed(self, packed: PackedDb, n_chunks: int = 64) -> dict:
+    def search_streamed(self, packed: PackedDb, n_chunks: int = 64,
+                        floor_from: torch.Tensor | None = None) -> dict:
         """End-to-end form for a host-resident (pinned) database, one kernel launch:
         the copy stream uploads chunk c (residues, starts, lengths, ids) and then
         its arrival flag; the striped kernel, launched at once, makes each task
@@ -279,7 +326,13 @@ class DatabaseSearch:
         order, sample = self._sampled_order(n, region=cj)
         if sample:
             o["_floor"].zero_()
-        self._launch16(n, floor=bool(sample), sample=sample, order=order,
+        if sample and floor_from is not None:  # a known lower bound: no sampling needed
+            o["_floor"].copy_(floor_from.reshape(1))
+            order, sample = None, 0
+            floor_on = True
+        else:
+            floor_on = bool(sample)
+        self._launch16(n, floor=floor_on, sample=sample, order=order,
                        feed=(self._arrived, cj, self._epoch))
         with torch.cuda.stream(copy):
             for c, (a, b, ra, rb) in enumerate(self._chunks):
@@ -291,6 +344,34 @@ class DatabaseSearch:
         cur.wait_stream(copy)  # ids before topk; the copy stream's work before the next step
         self._rescue(n)
         return o
+
+    def search_large(self, packed: PackedDb, max_residues: int, n_chunks: int = 64) -> torch.Tensor:
+        """Top-k over a database larger than the device buffers: passes of at most
+        ``max_residues`` residues (contiguous, so each pass stays length-sorted),
+        each streamed through one launch; the running top-k is merged on the
+        device, and from the second pass on its k-th score is the coordinate floor
+        (a lower bound of the final k-th best, so no sampling is needed).
+        Returns int64 [k, 4] records (score, target_id, ref_end, query_end)."""
+        assert self.prof is not None, "set_query() first"
+        lens = packed.length.numpy().astype(np.int64)
+        cum = np.concatenate([[0], np.cumsum(lens)])
+        best, kth = None, None
+        a = 0
+        while a < packed.n:
+            b = int(np.searchsorted(cum, cum[a] + max_residues, side="right")) - 1
+            b = max(b, a + 1)  # a single target larger than the budget still runs alone
+            ra, rb = int(cum[a]), int(cum[b])
+            start = packed.start[a:b] - ra
+            view = PackedDb(packed.codes[ra:rb], start.pin_memory() if packed.codes.is_pinned()
+                            else start, packed.length[a:b], packed.order[a:b] - a,
+                            packed.ids[a:b])
+            self.search_streamed(view, n_chunks, floor_from=kth)
+            top = self.topk(self.k)
+            best = top if best is None else select_topk(torch.cat([best, top]), self.k)
+            if best.shape[0] >= self.k:
+                kth = best[self.k - 1, 0].to(torch.int32)
+            a = b
+        return best
 
     def topk(self, k: int = 100) -> torch.Tensor:
         """k best (score desc, global id asc) as int64 [k, 4] on the device."""
@@ -307,6 +388,13 @@ def topk_records(score: torch.Tensor, ids: torch.Tensor, ref_end: torch.Tensor,
     _, idx = torch.topk(key, k, sorted=True)
     return torch.stack([score[idx].to(torch.int64), ids[idx].to(torch.int64),
                         ref_end[idx].to(torch.int64), query_end[idx].to(torch.int64)], dim=1)
+
+
+def select_topk(records: torch.Tensor, k: int) -> torch.Tensor:
+    """The k best of int64 [r, 4] records (score desc, target id asc)."""
+    key = (records[:, 0] << 32) | (0xFFFFFFFF - (records[:, 1] & 0xFFFFFFFF))
+    _, idx = torch.topk(key, min(k, records.shape[0]), sorted=True)
+    return records[idx]
 
 
 def merge_topk(records: torch.Tensor, k: int, group=None) -> torch.Tensor:

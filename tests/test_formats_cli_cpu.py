@@ -89,3 +89,31 @@ def test_scheme_from_matrix_file(tmp_path):
     alph, sch = runner._build_scheme(runner.RunConfig(matrix_path=str(f), gap_open=5,
                                                       gap_extend=2))
     assert alph.symbols == "AC" and sch == ScoringScheme(((2, -3), (-3, 2)), 5, 2)
+
+
+def test_packed_db_save_load_roundtrip(tmp_path):
+    from paper_1909_00899_b200 import search, workloads as W
+
+    w = W.config2(n_targets=500)
+    packed = search.pack(w.db, w.offsets, pin=False)
+    search.save_packed(str(tmp_path / "db"), packed, alphabet="stand-in")
+    back, meta = search.load_packed(str(tmp_path / "db"), pin=False)
+    assert meta["n"] == 500 and meta["residues"] == int(w.offsets[-1])
+    for name in search.PACKED_FILES:
+        assert (getattr(back, name).numpy() == getattr(packed, name).numpy()).all(), name
+    (tmp_path / "db" / "meta.json").write_text('{"format": "other"}')
+    import pytest
+
+    with pytest.raises(ValueError):
+        search.load_packed(str(tmp_path / "db"), pin=False)
+
+
+def test_shard_pairs_partition():
+    from paper_1909_00899_b200 import search
+
+    for n in (0, 1, 7, 1 << 20):
+        for world in (1, 2, 3, 8):
+            parts = [search.shard_pairs(n, r, world) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+            assert max(b - a for a, b in parts) - min(b - a for a, b in parts) <= 1

@@ -389,6 +389,25 @@ def test_long_query_database_overflow_rescue(A, oracle):
     assert (o["flags"].cpu().numpy()[ids == 5] & 4).all()  # rescued
 
 
+def test_database_larger_than_device_buffers(A):
+    """search_large (passes of a bounded residue budget, running top-k merged on the
+    device, floor carried between passes) returns the single-pass top-k exactly."""
+    from paper_1909_00899_b200 import search, workloads as W
+
+    w = W.config2(n_targets=30000)
+    packed = search.pack(w.db, w.offsets)
+    one = search.DatabaseSearch(w.scheme, coords="topk", k=50)
+    one.upload(packed)
+    one.set_query(w.query)
+    one.align()
+    want = one.topk(50).cpu().numpy()
+    eng = search.DatabaseSearch(w.scheme, coords="topk", k=50)
+    eng.set_query(w.query)
+    got = eng.search_large(packed, max_residues=packed.residues // 5 + 1).cpu().numpy()
+    assert (got == want).all()
+    assert (got[:, 2:] >= 0).all()
+
+
 def test_config4_scan_and_lazyf_identical(A, oracle):
     from paper_1909_00899_b200 import workloads as W
 
