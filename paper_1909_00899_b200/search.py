@@ -98,10 +98,12 @@ def load_packed(path: str, pin: bool = True) -> tuple[PackedDb, dict]:
     if meta.get("format") != "b200-swscan-packed-db":
         raise ValueError(f"{path}: not a packed database")
 
-    def t(name):
+    def t(name):  # one copy from the memory-mapped file into (pinned) host memory
         a = np.load(os.path.join(path, name + ".npy"), mmap_mode="r")
-        x = torch.from_numpy(np.ascontiguousarray(a))
-        return x.pin_memory() if pin and torch.cuda.is_available() else x
+        x = torch.empty(a.shape, dtype=torch.from_numpy(np.empty(0, a.dtype)).dtype,
+                        pin_memory=pin and torch.cuda.is_available())
+        x.numpy()[...] = a
+        return x
 
     packed = PackedDb(*(t(name) for name in PACKED_FILES))
     if packed.n != meta["n"]:
