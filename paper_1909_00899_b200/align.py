@@ -369,10 +369,9 @@ def align_prebuilt(kernel: str, prof: DeviceProfile, bias=None, ref=None,
                             prof.lanes if prof.plan16 else 0, 0, 0, -1, -1, None)
     long_query = prof.plan16 is None
     if not long_query and prof.plan32 is None:
-        try:
-            prof.ensure32()
-        except _lib.SwError:
-            long_query = None  # 16-bit warp kernel; a rescue would need the strip pipeline
+        prof.ensure32()
+        if prof.long32:
+            long_query = None  # 16-bit warp kernel; a rescue needs the strip pipeline
     if long_query:
         if kernel != "scan":
             raise _lib.SwError(_lib.SW_ENOTSUP,
@@ -394,7 +393,7 @@ def align_prebuilt(kernel: str, prof: DeviceProfile, bias=None, ref=None,
         out = db_align(prof, tgt, start, length, None, kernel, passes)
     flags = int(out["flags"][0])
     if flags & _lib.FLAG_RESCUED:
-        P, L_ = prof.plan32.lanes, prof.plan32.seg_len
+        P, L_ = (prof.plan32.lanes, prof.plan32.seg_len) if prof.plan32 is not None else (0, 0)
     else:
         pl = prof.for_kernel(kernel)[0]
         P, L_ = pl.lanes, pl.seg_len

@@ -358,9 +358,12 @@ sw_striped_kernel(const SwArgs a) {
   const bool no_coords = a.ref_end == nullptr && a.query_end == nullptr;
   const int64_t fs_tasks = (has_floor && a.task_ctr) ? min((a.floor_sample + G - 1) / G, n_tasks) : 0;
 #ifndef SWB_KCH
-#define SWB_KCH 8
+#define SWB_KCH 0  // 0: by segment length (see kCh)
 #endif
-  constexpr int kCh = SWB_KCH, kNch = (LMAX + kCh - 1) / kCh;
+  // chunk of the running column maxima (a position search scans one chunk):
+  // 16 words for the long exact segments (fewer maxima to combine per column)
+  constexpr int kCh = SWB_KCH > 0 ? SWB_KCH : (EXACT && LMAX > 32 ? 16 : 8);
+  constexpr int kNch = (LMAX + kCh - 1) / kCh;
 
   // Task claiming: with a counter, warps take the next task (in length-descending
   // order) when they finish one -- longest-first greedy, so the warps end together
