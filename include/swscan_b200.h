@@ -156,6 +156,27 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
                       int32_t* d_ref_end, int32_t* d_query_end, uint8_t* d_flags,
                       sw_stream_t stream);
 
+/* One alignment across a CTA or a thread-block cluster at high stripe counts: the
+ * reference layout VectorSpec(p) for p beyond one warp (up to 32,768 16-bit /
+ * 16,384 32-bit stripes), with Alg. 6's F scan resolved warp shuffle -> block
+ * (shared memory + one bar.sync per column) -> cluster (distributed shared memory,
+ * CTAs pipelined along the query).  Reference: align_pair(kernel, p, query, ref,
+ * scheme) / align_prebuilt, src/_compiled.py:588-615, for p the reference accepts
+ * (power of two).  Lazy-F kernels (SW_KERNEL_LAZYF*) run on one CTA (p <= 2,048
+ * 16-bit / 1,024 32-bit), one block-wide vote per pass; d_col_passes (int32 [n])
+ * and d_pass_stats (int64 [2]: total passes, early-exit columns) are nullable.
+ * lanes = 0 chooses the layout.  sw_block_plan reports it: out[4] = {lanes,
+ * threads per CTA, CTAs per cluster, seg_len}.  coords = 0 skips the end-coordinate
+ * search (ref_end = query_end = -1). */
+int32_t sw_block_plan(int32_t width, int32_t kernel, int64_t m, int32_t n_sym, int32_t lanes,
+                      int32_t* out);
+int32_t sw_align_block(int32_t width, int32_t kernel, int32_t lanes, const uint8_t* d_query,
+                       int64_t m, const uint8_t* d_ref, int64_t n, const int8_t* d_sub,
+                       int32_t n_sym, int32_t gap_open, int32_t gap_extend, int32_t bias,
+                       int32_t max_sub, int32_t coords, int32_t* d_score, int32_t* d_ref_end,
+                       int32_t* d_query_end, uint8_t* d_flags, int32_t* d_col_passes,
+                       int64_t* d_pass_stats, sw_stream_t stream);
+
 /* Gather the ids of alignments whose flags intersect `mask` into d_list and
  * their count into *d_count (device int64).  Used to re-run 16-bit overflow
  * suspects in 32 bits without a host round trip. */

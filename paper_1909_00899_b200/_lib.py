@@ -37,6 +37,8 @@ EXPORTS = (
     "sw_dpx_probe",
     "sw_long_workspace_bytes",
     "sw_align_long",
+    "sw_block_plan",
+    "sw_align_block",
 )
 
 
@@ -133,6 +135,11 @@ def load():
     L.sw_align_long.restype = i32
     L.sw_align_long.argtypes = [i32, i32, vp, i64, vp, i64, vp, i32, i32, i32, i32, i32, vp, i64,
                                 vp, vp, vp, vp, vp]
+    L.sw_block_plan.restype = i32
+    L.sw_block_plan.argtypes = [i32, i32, i64, i32, i32, C.POINTER(C.c_int32)]
+    L.sw_align_block.restype = i32
+    L.sw_align_block.argtypes = [i32, i32, i32, vp, i64, vp, i64, vp, i32, i32, i32, i32, i32, i32,
+                                 vp, vp, vp, vp, vp, vp, vp]
     _lib = _Strict(L)
     return _lib
 
@@ -173,3 +180,14 @@ def plan_query(m: int, n_sym: int, width: int, lanes: int = 0) -> Plan:
     p = Plan()
     check(load().sw_plan_query(int(m), int(n_sym), int(width), int(lanes), C.byref(p)))
     return p
+
+
+def block_plan(m: int, n_sym: int, width: int = 16, kernel: int = 2, lanes: int = 0):
+    """Layout of the block / cluster kernel: (lanes, threads per CTA, CTAs per cluster,
+    seg_len), or None when no layout exists (sw_block_plan)."""
+    out = (C.c_int32 * 4)()
+    rc = load().sw_block_plan(int(width), int(kernel), int(m), int(n_sym), int(lanes), out)
+    if rc == SW_ENOTSUP:
+        return None
+    check(rc)
+    return tuple(int(x) for x in out)

@@ -262,6 +262,61 @@ def align_long(query, ref, scheme: ScoringScheme, width: int = 32, kernel: str =
     return {"score": o[0], "ref_end": o[1], "query_end": o[2], "flags": flags & ~_lib.FLAG_RESCUE}
 
 
+def align_block(query, ref, scheme: ScoringScheme, p: int = 0, kernel: str = "scan",
+                width: int = 16, coords: bool = True, col_passes: bool = False,
+                query_dev: torch.Tensor | None = None, ref_dev: torch.Tensor | None = None) -> dict:
+    """One pair on the block / cluster kernel (sw_align_block): the reference layout
+    VectorSpec(p) for p beyond one warp, the F scan resolved warp -> block -> cluster
+    (DSMEM). ``p = 0`` chooses the layout. Returns host values ``score, ref_end,
+    query_end, flags, lanes, threads, cluster, seg_len`` (+ ``col_passes``,
+    ``pass_stats`` for lazy-F); a 16-bit run that hits the wrap guard is repeated in
+    32 bits."""
+    _require_cuda()
+    L = _lib.load()
+    kid = _kernel_id(kernel)
+    if kid == _lib.KERNEL_IDS["wavefront"]:
+        raise _lib.SwError(_lib.SW_ENOTSUP, "the block kernel runs scan and lazy-F")
+    qd = query_dev if query_dev is not None else torch.from_numpy(
+        _codes(query, scheme.n_symbols, "query")).cuda()
+    rd = ref_dev if ref_dev is not None else torch.from_numpy(
+        _codes(ref, scheme.n_symbols, "reference")).cuda()
+    m, n = int(qd.numel()), int(rd.numel())
+    if m == 0 or n == 0:
+        return {"score": 0, "ref_end": -1, "query_end": -1, "flags": 0}
+    sub = torch.from_numpy(scheme.as_array()).cuda()
+    out = torch.zeros(4, dtype=torch.int32, device="cuda")
+    fl = torch.zeros(1, dtype=torch.uint8, device="cuda")
+    passes = torch.zeros(n, dtype=torch.int32, device="cuda") if col_passes else None
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda") if kernel != "scan" else None
+    res = {}
+    for w in ((16, 32) if width == 16 else (32,)):
+        geo = _lib.block_plan(m, scheme.n_symbols, w, kid, p)
+        if geo is None:
+            if w == 32 and width == 16:
+                geo = _lib.block_plan(m, scheme.n_symbols, 32, kid, 0)  # rescue at any layout
+            if geo is None:
+                raise _lib.SwError(_lib.SW_ENOTSUP, f"no block layout for m={m}, p={p}, width={w}")
+        _lib.check(L.sw_align_block(w, kid, geo[0], _ptr(qd), m, _ptr(rd), n, _ptr(sub),
+                                    scheme.n_symbols, scheme.gap_open, scheme.gap_extend,
+                                    scheme.bias, scheme.max_score, int(bool(coords)),
+                                    C.c_void_p(out.data_ptr()), C.c_void_p(out.data_ptr() + 4),
+                                    C.c_void_p(out.data_ptr() + 8), _ptr(fl), _ptr(passes),
+                                    _ptr(stats), _stream()))
+        flags = int(fl.item())
+        res = {"lanes": geo[0], "threads": geo[1], "cluster": geo[2], "seg_len": geo[3]}
+        if not flags & _lib.FLAG_RESCUE:
+            break
+    o = out.cpu().tolist()
+    if width == 16 and w == 32:
+        flags |= _lib.FLAG_RESCUED
+    res.update(score=o[0], ref_end=o[1], query_end=o[2], flags=flags & ~_lib.FLAG_RESCUE)
+    if passes is not None:
+        res["col_passes"] = passes.cpu().numpy()
+    if stats is not None:
+        res["pass_stats"] = tuple(int(x) for x in stats.cpu().tolist())
+    return res
+
+
 def db_align(prof: DeviceProfile, tgt: torch.Tensor, start: torch.Tensor, length: torch.Tensor,
              order: torch.Tensor | None = None, kernel: str = "scan",
              col_passes: torch.Tensor | None = None, out: dict | None = None,
@@ -367,6 +422,13 @@ def align_prebuilt(kernel: str, prof: DeviceProfile, bias=None, ref=None,
     if n == 0:
         return _result_from(None, kernel, 0, prof.seg_len if prof.plan16 else 0,
                             prof.lanes if prof.plan16 else 0, 0, 0, -1, -1, None)
+    if prof.requested_lanes > 64 and _lib.block_plan(prof.m, prof.scheme.n_symbols, 16, kid,
+                                                     prof.requested_lanes) is not None:
+        # the reference layout VectorSpec(p) beyond one warp: block / cluster kernel
+        o = align_block(None, r, prof.scheme, prof.requested_lanes, kernel, 16,
+                        col_passes=kernel != "scan", query_dev=prof.query)
+        return _result_from(prof, kernel, n, o["seg_len"], o["lanes"], o["score"], o["flags"],
+                            o["ref_end"], o["query_end"], o.get("col_passes"))
     long_query = prof.plan16 is None
     if not long_query and prof.plan32 is None:
         prof.ensure32()

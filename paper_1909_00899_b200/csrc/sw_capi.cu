@@ -11,6 +11,7 @@
 #include <mutex>
 
 #include "sw_chain.cuh"
+#include "sw_block.cuh"
 #include "../../include/swscan_b200.h"
 
 using namespace swb;
@@ -35,7 +36,8 @@ KernelTable g_tab[2][3];
 ExactTable g_exact;  // 16-bit scan, exact segment length
 const void* g_chain[2][6];  // strip pipeline [width][L = 1, 2, 4, 8, 16, 32]
 const void* g_chain_prof[2];
-const void* g_wave[4];  // strip pipeline, intra-strip wavefront [L = 1, 2, 4, 8]
+const void* g_wave[4];
+const void* g_block[2][3][16];  // block / cluster scan [width][variant][L-1]  // strip pipeline, intra-strip wavefront [L = 1, 2, 4, 8]
 std::once_flag g_once;
 
 void init_tables() {
@@ -57,6 +59,8 @@ void init_tables() {
   swb_fill_exact_t4_g0_f(g_exact); swb_fill_exact_t4_g1_f(g_exact); swb_fill_exact_t4_g2_f(g_exact);
   swb_fill_chain(g_chain, g_chain_prof);
   swb_fill_wave(g_wave);
+  swb_fill_block16(g_block[0]);
+  swb_fill_block32(g_block[1]);
   swb_fill_w16_scan(g_tab[0][VAR_SCAN]);
   swb_fill_w16_lazyf(g_tab[0][VAR_LAZYF]);
   swb_fill_w16_mirror(g_tab[0][VAR_LAZYF_MIRROR]);
@@ -72,6 +76,43 @@ int ilog2(int x) {
 }
 
 bool pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+// ---- block / cluster kernel geometry ----
+struct BlockGeo {
+  int lanes, nt, cl, L;
+  size_t smem;
+};
+int block_max_threads(int L) { return L <= 4 ? 1024 : (L <= 8 ? 512 : 256); }
+size_t block_smem(int A, int L, int nt) {
+  return (size_t)(A + 1) * L * nt * 4 + 64 * 16 + (kBlockRing + 2) * 8 + 32 * 16;
+}
+constexpr size_t kMaxDynSmem = 227 * 1024;
+// layout for `lanes` stripes (a power of two): CTAs per cluster doubled until a CTA
+// fits the thread and shared-memory limits; lazy-F needs a single CTA
+bool block_geo_for(int width, bool scan, int64_t m, int A, int lanes, BlockGeo* g) {
+  const int lpw = width == 16 ? 2 : 1;
+  if (!pow2(lanes) || lanes < 32 * lpw) return false;
+  const int64_t L = (m + lanes - 1) / lanes;
+  if (L < 1 || L > 16) return false;
+  const int T = lanes / lpw;
+  int cl = 1;
+  while (cl <= 16 && (T / cl > block_max_threads((int)L) || block_smem(A, (int)L, T / cl) > kMaxDynSmem)) cl *= 2;
+  if (cl > 16 || T / cl < 32 || (!scan && cl > 1)) return false;
+  g->lanes = lanes; g->nt = T / cl; g->cl = cl; g->L = (int)L;
+  g->smem = block_smem(A, (int)L, g->nt);
+  return true;
+}
+// lanes = 0: scan -- the fewest stripes with segments of <= 4 words (more threads cost
+// the per-column scan little; longer segments cost every column), else <= 16;
+// lazy-F -- the fewest stripes that fit one CTA (every pass shifts F by one lane)
+bool block_geo(int width, bool scan, int64_t m, int A, int lanes, BlockGeo* g) {
+  if (lanes) return block_geo_for(width, scan, m, A, lanes, g);
+  const int lpw = width == 16 ? 2 : 1;
+  for (int lmax : {4, 16})
+    for (int p = 32 * lpw; p <= 16 * 1024 * lpw; p *= 2)
+      if ((m + p - 1) / p <= (scan ? lmax : 16) && block_geo_for(width, scan, m, A, p, g)) return true;
+  return false;
+}
 
 int lmax_index(int L) {
   for (int i = 0; i < kNumLmax; ++i)
@@ -656,6 +697,74 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
   void* params[] = {(void*)&a};
   e = cudaLaunchCooperativeKernel(fn, dim3(g.nb), dim3(32), params, smem, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchCooperativeKernel(sw_chain_kernel)");
+  return SW_OK;
+}
+
+int32_t sw_block_plan(int32_t width, int32_t kernel, int64_t m, int32_t n_sym, int32_t lanes,
+                      int32_t* out) {
+  if (!out) return fail(SW_EINVAL, "NULL argument");
+  if (width != 16 && width != 32) return fail(SW_EINVAL, "width must be 16 or 32");
+  if (kernel < SW_KERNEL_LAZYF || kernel > SW_KERNEL_LAZYF_NOEXIT_MIRROR) return fail(SW_EINVAL, "kernel %d", kernel);
+  if (m < 1) return fail(SW_EINVAL, "empty query");
+  if (n_sym < 1 || n_sym > kMaxSym) return fail(SW_ENOTSUP, "alphabet size %d", n_sym);
+  BlockGeo g;
+  if (!block_geo(width, kernel == SW_KERNEL_SCAN, m, n_sym, lanes, &g))
+    return fail(SW_ENOTSUP, "no block layout for m=%lld lanes=%d width=%d kernel=%d", (long long)m, lanes,
+                width, kernel);
+  out[0] = g.lanes; out[1] = g.nt; out[2] = g.cl; out[3] = g.L;
+  return SW_OK;
+}
+
+int32_t sw_align_block(int32_t width, int32_t kernel, int32_t lanes, const uint8_t* d_query,
+                       int64_t m, const uint8_t* d_ref, int64_t n, const int8_t* d_sub,
+                       int32_t n_sym, int32_t gap_open, int32_t gap_extend, int32_t bias,
+                       int32_t max_sub, int32_t coords, int32_t* d_score, int32_t* d_ref_end,
+                       int32_t* d_query_end, uint8_t* d_flags, int32_t* d_col_passes,
+                       int64_t* d_pass_stats, sw_stream_t stream) {
+  std::call_once(g_once, init_tables);
+  if (!d_query || !d_ref || !d_sub || !d_score) return fail(SW_EINVAL, "NULL argument");
+  int32_t geo[4];
+  int32_t rc = sw_block_plan(width, kernel, m, n_sym, lanes, geo);
+  if (rc != SW_OK) return rc;
+  if (!(gap_open >= gap_extend && gap_extend >= 1)) return fail(SW_EINVAL, "require gap_open >= gap_extend >= 1");
+  if (n < 1) return fail(SW_EINVAL, "empty reference");
+  if (n > (1LL << 31) - 2) return fail(SW_ENOTSUP, "reference longer than 2^31");
+  BlockGeo g;
+  block_geo(width, kernel == SW_KERNEL_SCAN, m, n_sym, lanes, &g);
+  const int var = kernel == SW_KERNEL_SCAN ? VAR_SCAN
+                  : (kernel == SW_KERNEL_LAZYF_MIRROR || kernel == SW_KERNEL_LAZYF_NOEXIT_MIRROR) ? VAR_LAZYF_MIRROR
+                                                                                                   : VAR_LAZYF;
+  const void* fn = g_block[width == 16 ? 0 : 1][var][g.L - 1];
+  BlockArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.query = d_query; a.sub = d_sub; a.n_sym = n_sym; a.m = (int)m; a.seg_len = g.L;
+  a.ref = d_ref; a.n = n; a.go = gap_open; a.ge = gap_extend; a.bias = bias; a.max_sub = max_sub;
+  a.early_exit = (kernel == SW_KERNEL_LAZYF || kernel == SW_KERNEL_LAZYF_MIRROR) ? 1 : 0;
+  a.coords = coords ? 1 : 0;
+  a.score = d_score; a.ref_end = d_ref_end; a.query_end = d_query_end; a.flags = d_flags;
+  a.col_passes = d_col_passes; a.pass_stats = d_pass_stats;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(block smem)");
+  if (g.cl > 8) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(non-portable cluster)");
+  }
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3(g.cl);
+  cfg.blockDim = dim3(g.nt);
+  cfg.dynamicSmemBytes = g.smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = g.cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* params[] = {(void*)&a};
+  e = cudaLaunchKernelExC(&cfg, fn, params);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernelEx(sw_block_kernel)");
   return SW_OK;
 }
 

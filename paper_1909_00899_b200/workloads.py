@@ -111,6 +111,10 @@ class PairWorkload:
     notes: dict = field(default_factory=dict)
 
     @property
+    def m(self) -> int:
+        return int(self.query.shape[0])
+
+    @property
     def cells(self) -> int:
         return int(self.query.shape[0]) * int(self.ref.shape[0])
 
