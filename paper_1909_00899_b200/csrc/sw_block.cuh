@@ -156,13 +156,14 @@ __global__ void __launch_bounds__(L <= 4 ? 1024 : (L <= 8 ? 512 : 256), 1) sw_bl
   for (int k = 0; k < kNch; ++k) cmk[k] = 0u;
   int64_t tot_passes = 0, breaks = 0;
   int par = 0;                       // parity of the shared-memory publication slots
-  unsigned long long cons_seen = 0;  // last observed progress of CTA rank+1
+  unsigned cons_seen = 0;  // last observed progress of CTA rank+1
   const int P = (int)CL * NT * LPW;
   int nxt = n > 0 ? (int)__ldg(a.ref) : 0;
 
-  for (int64_t i = 0; i < n; ++i) {
+  const int n32 = (int)n;  // host guarantees n < 2^31
+  for (int i = 0; i < n32; ++i) {
     const int sym = nxt;
-    nxt = (i + 1 < n) ? (int)__ldg(a.ref + i + 1) : 0;
+    nxt = (i + 1 < n32) ? (int)__ldg(a.ref + i + 1) : 0;
     const uint32_t* pr = prof_s + sym * (L * NT) + tid;
     // diagonal input of each lane: the previous lane's corrected last H (shift by one lane)
     uint32_t r = __shfl_up_sync(FULL, wcorr, 1);
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(L <= 4 ? 1024 : (L <= 8 ? 512 : 256), 1) sw_bl
               }
             }
             bv = cv;
-            bcol = (int)i;
+            bcol = i;
             bq = (LPW * g + h) * L + jj;
           }
         }
@@ -235,14 +236,14 @@ __global__ void __launch_bounds__(L <= 4 ? 1024 : (L <= 8 ? 512 : 256), 1) sw_bl
       int cin = 0, win = 0;
       if (rank > 0) {
         // the previous CTA's column-i boundary (inclusive F prefix, corrected last H)
-        const unsigned want = (((unsigned)(i / kBlockRing)) & 1u) ^ 1u;
-        const uint32_t addr = ring_base + (uint32_t)(i % kBlockRing) * 8u;
+        const unsigned want = (((unsigned)i / kBlockRing) & 1u) ^ 1u;
+        const uint32_t addr = ring_base + ((unsigned)i % kBlockRing) * 8u;
         unsigned long long v = ld_local_u64(addr);
         while ((((unsigned)(v >> 31)) & 1u) != want || (((unsigned)(v >> 63)) & 1u) != want)
           v = ld_local_u64(addr);
         cin = (int)((uint32_t)v & 0x7fffffffu);
         win = (int)((uint32_t)(v >> 32) & 0x7fffffffu);
-        if (tid == 0 && (i % (kBlockRing / 4)) == kBlockRing / 4 - 1)
+        if (tid == 0 && ((unsigned)i % (kBlockRing / 4)) == kBlockRing / 4 - 1)
           st_cluster_u64(cons_addr, rank - 1, (unsigned long long)(i + 1));
       }
       const int ak = lane < w ? agg[par * 32 + lane].x : 0;
@@ -266,17 +267,17 @@ __global__ void __launch_bounds__(L <= 4 ? 1024 : (L <= 8 ? 512 : 256), 1) sw_bl
       }
       // the CTA's boundary for CTA rank+1: inclusive prefix and corrected last H
       if (rank + 1 < CL && w == NW - 1) {
-        if (i >= (int64_t)kBlockRing && cons_seen + kBlockRing <= (unsigned long long)i) {
-          const unsigned long long need = (unsigned long long)(i - kBlockRing + 1);
-          unsigned long long c = ld_local_u64(cons_addr);
-          while (c < need) c = ld_local_u64(cons_addr);
+        if (cons_seen + kBlockRing <= (unsigned)i) {
+          const unsigned need = (unsigned)i - kBlockRing + 1;
+          unsigned c = (unsigned)ld_local_u64(cons_addr);
+          while (c < need) c = (unsigned)ld_local_u64(cons_addr);
           cons_seen = c;
         }
         if (lane == 31) {
-          const unsigned tag = (((unsigned)(i / kBlockRing)) & 1u) ^ 1u;
+          const unsigned tag = (((unsigned)i / kBlockRing) & 1u) ^ 1u;
           const uint32_t so = (uint32_t)__viaddmax_s32_relu(bex, -D, Ag) | (tag << 31);
           const uint32_t wo = (uint32_t)Wd::get(wcorr, LPW - 1) | (tag << 31);
-          st_cluster_u64(ring_base + (uint32_t)(i % kBlockRing) * 8u, rank + 1,
+          st_cluster_u64(ring_base + ((unsigned)i % kBlockRing) * 8u, rank + 1,
                          ((unsigned long long)wo << 32) | so);
         }
       }
