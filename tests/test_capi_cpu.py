@@ -59,6 +59,35 @@ def test_plan_reproduces_reference_layout():
         _lib.plan_query(10, 4, 16, 6)
 
 
+def test_block_plan_reference_layouts():
+    """Host-side geometry of the block / cluster kernel (sw_block_plan): the
+    reference layout VectorSpec(p) beyond one warp, CTAs per cluster chosen to fit
+    the per-CTA thread and shared-memory limits, lazy-F on one CTA only."""
+    from paper_1909_00899_b200 import _lib
+
+    _lib.build()
+    scan, lazy = _lib.KERNEL_IDS["scan"], _lib.KERNEL_IDS["lazyf"]
+    for m, p, width, want in ((2048, 2048, 16, (2048, 1024, 1, 1)),
+                              (2048, 256, 16, (256, 128, 1, 8)),
+                              (65536, 16384, 32, (16384, 1024, 16, 4)),
+                              (65536, 4096, 32, (4096, 256, 16, 16)),
+                              (8192, 16384, 16, (16384, 1024, 8, 1)),
+                              (1000, 128, 32, (128, 128, 1, 8))):
+        assert _lib.block_plan(m, 4, width, scan, p) == want, (m, p, width)
+    # L = ceil(m / p) must be 1..16; p a power of two of at least one warp pair
+    assert _lib.block_plan(4096, 4, 16, scan, 128) is None
+    assert _lib.block_plan(100, 4, 16, scan, 96) is None
+    assert _lib.block_plan(100, 4, 16, scan, 32) is None
+    # lazy-F: one CTA (p <= 2,048 16-bit / 1,024 32-bit)
+    assert _lib.block_plan(2048, 20, 16, lazy, 2048) == (2048, 1024, 1, 1)
+    assert _lib.block_plan(2048, 20, 32, lazy, 2048) is None
+    # a 20-letter profile of 4 words x 1,024 threads exceeds one CTA's shared memory
+    assert _lib.block_plan(65536, 20, 32, scan, 16384) is None
+    # automatic layout: scan prefers <= 4-word segments, lazy-F the fewest stripes
+    assert _lib.block_plan(2048, 20, 16, scan, 0) == (512, 256, 1, 4)
+    assert _lib.block_plan(2048, 20, 16, lazy, 0) == (128, 64, 1, 16)
+
+
 def test_counters_closed_form_matches_reference_tallies(oracle):
     """Host reconstruction of the reference's op counters from pass counts."""
     from paper_1909_00899_b200.align import counters_from_passes
