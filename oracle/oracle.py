@@ -74,6 +74,14 @@ def lib():
         L.swo_batch_striped.argtypes = [C.c_int32, C.c_int64, C.c_int64, _u8p, _i64p, _u8p, _i64p,
                                         vp, C.c_int32, C.c_int64, C.c_int64, vp, vp, vp, vp,
                                         _i64p, _u8p, _i64p, C.c_int32]
+        L.swo_start_coords.restype = C.c_int32
+        L.swo_start_coords.argtypes = [_u8p, _u8p, _i8p, C.c_int32, C.c_int64, C.c_int64,
+                                       C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_int32)]
+        L.swo_batch_starts.restype = None
+        L.swo_batch_starts.argtypes = [C.c_int64, _u8p, _i64p, _u8p, _i64p, _i8p, C.c_int32,
+                                       C.c_int64, C.c_int64, _i64p, _i32p, _i32p, _i32p, _i32p,
+                                       C.c_int32]
         L.swo_db_striped.restype = None
         L.swo_db_striped.argtypes = [C.c_int32, _u16p, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                      _u8p, _i64p, C.c_int64, C.c_int64, _i64p, _u8p, C.c_int32]
@@ -217,3 +225,35 @@ def db_striped(kernel: str, prof: np.ndarray, bias: int, flat_r, r_off, go: int,
     lib().swo_db_striped(KERNEL_IDS[kernel], prof.reshape(-1), L, p, bias, n, fr, ro, go, ge,
                          score, over, threads or n_threads())
     return score, over
+
+
+def start_coords(query, ref, sub, go: int, ge: int, score: int, ref_end: int,
+                 query_end: int) -> tuple[int, int]:
+    """(ref_start, query_start) of the optimal alignment ending at the end cell
+    (swo_start_coords); (-1, -1) for score 0."""
+    rs, qs = C.c_int32(), C.c_int32()
+    q, r = _u8(query), _u8(ref)
+    if score > 0 and (ref_end >= r.shape[0] or query_end >= q.shape[0]):
+        raise ValueError("end cell outside the sequences")
+    rc = lib().swo_start_coords(q if q.size else np.zeros(1, np.uint8),
+                                r if r.size else np.zeros(1, np.uint8), _i8(sub),
+                                int(np.asarray(sub).shape[0]), go, ge, int(score), int(ref_end),
+                                int(query_end), C.byref(rs), C.byref(qs))
+    if rc != 0:
+        raise ValueError("no alignment from the end cell reaches the score")
+    return rs.value, qs.value
+
+
+def batch_starts(flat_q, q_off, flat_r, r_off, sub, go: int, ge: int, score, ref_end, query_end,
+                 threads: int | None = None) -> tuple[np.ndarray, np.ndarray]:
+    n = int(np.asarray(q_off).shape[0] - 1)
+    rs = np.zeros(n, np.int32)
+    qs = np.zeros(n, np.int32)
+    fq, fr = _u8(flat_q), _u8(flat_r)
+    lib().swo_batch_starts(n, fq if fq.size else np.zeros(1, np.uint8), _i64(q_off),
+                           fr if fr.size else np.zeros(1, np.uint8), _i64(r_off), _i8(sub),
+                           int(np.asarray(sub).shape[0]), go, ge, _i64(score),
+                           np.ascontiguousarray(ref_end, dtype=np.int32),
+                           np.ascontiguousarray(query_end, dtype=np.int32), rs, qs,
+                           threads or n_threads())
+    return rs, qs

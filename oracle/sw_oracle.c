@@ -404,3 +404,73 @@ void swo_db_striped(int32_t kernel_id, const uint16_t *prof, int64_t L, int64_t 
         if (overflow) overflow[t] = sat;
     }
 }
+
+/* ---- start coordinates (extension: SURVEY 8(f) item 4; the reference lists
+ *      traceback as a non-goal) ----
+ * Given the score and first-max end cell of an optimal local alignment, the
+ * start is found by an anchored Gotoh DP over the reversed prefixes (reversed
+ * reference index i' = ref_end - i outer, reversed query index q' = query_end - q
+ * inner) whose only start is the end pair itself: no clamping at 0, boundary
+ * -inf except the virtual origin.  The first cell in that loop order whose
+ * anchored score equals `score` is the alignment's first aligned pair, i.e. the
+ * start of the optimal alignment ending at the end cell that is shortest in the
+ * reference, ties to the largest query start.  Such a cell is a diagonal cell
+ * (a gap cell is strictly below its predecessor).  Returns 0, or -1 when no
+ * anchored alignment reaches `score` (inconsistent inputs). */
+int32_t swo_start_coords(const uint8_t *query, const uint8_t *ref, const int8_t *sub,
+                         int32_t n_sym, int64_t go, int64_t ge, int64_t score, int32_t ref_end,
+                         int32_t query_end, int32_t *ref_start, int32_t *query_start) {
+    *ref_start = -1;
+    *query_start = -1;
+    if (score <= 0 || ref_end < 0 || query_end < 0) return score <= 0 ? 0 : -1;
+    const int64_t NEG = -((int64_t)1 << 60);
+    const int64_t mq = (int64_t)query_end + 1, nr = (int64_t)ref_end + 1;
+    int64_t *h = (int64_t *)malloc((size_t)(mq + 1) * sizeof(int64_t));  /* h[k]: q' = k-1 */
+    int64_t *e = (int64_t *)malloc((size_t)(mq + 1) * sizeof(int64_t));
+    for (int64_t k = 0; k <= mq; k++) { h[k] = NEG; e[k] = NEG; }
+    h[0] = 0; /* row i' = -1: the virtual origin, diagonal of (0, 0) */
+    int32_t rc = -1;
+    for (int64_t ip = 0; ip < nr && rc < 0; ip++) {
+        const int8_t *row = sub + (int64_t)ref[ref_end - ip] * n_sym;
+        int64_t diag = h[0];
+        h[0] = NEG; /* column q' = -1 for rows i' >= 0 */
+        int64_t f = NEG, hleft = NEG;
+        for (int64_t k = 1; k <= mq; k++) {
+            int64_t ev = e[k] - ge, t = h[k] - go;
+            if (t > ev) ev = t;
+            int64_t fv = f - ge;
+            t = hleft - go;
+            if (t > fv) fv = t;
+            int64_t u = diag + (int64_t)row[query[query_end - (k - 1)]];
+            int64_t hv = u;
+            if (ev > hv) hv = ev;
+            if (fv > hv) hv = fv;
+            diag = h[k];
+            h[k] = hv;
+            e[k] = ev;
+            f = fv;
+            hleft = hv;
+            if (hv == score) {
+                *ref_start = (int32_t)(ref_end - ip);
+                *query_start = (int32_t)(query_end - (k - 1));
+                rc = 0;
+                break;
+            }
+        }
+    }
+    free(h);
+    free(e);
+    return rc;
+}
+
+/* Batch form: pair t = (query t, target t) of CSR inputs with its hit. */
+void swo_batch_starts(int64_t npairs, const uint8_t *flat_q, const int64_t *q_off,
+                      const uint8_t *flat_r, const int64_t *r_off, const int8_t *sub,
+                      int32_t n_sym, int64_t go, int64_t ge, const int64_t *score,
+                      const int32_t *ref_end, const int32_t *query_end, int32_t *ref_start,
+                      int32_t *query_start, int32_t nthreads) {
+#pragma omp parallel for schedule(dynamic, 16) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int64_t t = 0; t < npairs; t++)
+        swo_start_coords(flat_q + q_off[t], flat_r + r_off[t], sub, n_sym, go, ge, score[t],
+                         ref_end[t], query_end[t], ref_start + t, query_start + t);
+}

@@ -607,6 +607,87 @@ def pairs_align(flat_q, q_off, flat_r, r_off, *, kernel: str = "scan", lanes: in
     return res
 
 
+def align_starts(flat_q, q_off, flat_r, r_off, scheme: ScoringScheme, score, ref_end,
+                 query_end, width: int = 16) -> tuple[np.ndarray, np.ndarray]:
+    """Start coordinates of optimal local alignments (the
+    reference has no traceback): for each pair with its exact
+    ``score`` and first-max end cell, the 0-based ``(ref_start, query_start)`` of
+    the optimal alignment ending there that is shortest in the reference (ties:
+    largest query start); ``(-1, -1)`` for score 0 or an unlocated end (-2).
+
+    Device method: one pairs launch over the reversed prefixes
+    ``query[query_end::-1]`` / ``ref[ref_end::-1]``, each preceded by a run of
+    ``r = ceil((score + 1) / 127)`` copies of an extra symbol X scoring +127
+    against itself and -127 against everything else. Every alignment through all
+    r X pairs scores ``127 r + (anchored score from the end pair)`` and every other
+    alignment scores below ``127 r``, so the first cell reaching
+    ``127 r + score`` in the kernel's reference-major order is the alignment's
+    first pair -- the same rule as the oracle's anchored reverse DP
+    (oracle/sw_oracle.c swo_start_coords). Exactness is checked: the launch must
+    return exactly ``127 r + score``."""
+    q_off = np.asarray(q_off, dtype=np.int64)
+    r_off = np.asarray(r_off, dtype=np.int64)
+    sc = np.asarray(score, dtype=np.int64)
+    re_ = np.asarray(ref_end, dtype=np.int64)
+    qe = np.asarray(query_end, dtype=np.int64)
+    n = int(q_off.shape[0] - 1)
+    rs = np.full(n, -1, np.int32)
+    qs = np.full(n, -1, np.int32)
+    sel = np.nonzero((sc > 0) & (re_ >= 0) & (qe >= 0))[0]
+    if sel.size == 0:
+        return rs, qs
+    A = scheme.n_symbols
+    if A + 1 > 32:
+        raise _lib.SwError(_lib.SW_ENOTSUP, "start coordinates need an alphabet of <= 31 symbols")
+    if np.any(re_[sel] >= np.diff(r_off)[sel]) or np.any(qe[sel] >= np.diff(q_off)[sel]):
+        raise ValueError("end cell outside the sequences")
+    fq = _codes(flat_q, A, "query")
+    fr = _codes(flat_r, A, "reference")
+    reps = (sc[sel] + 1 + 126) // 127
+
+    def reversed_ext(flat, off, end):
+        lens = reps + end[sel] + 1
+        o = np.zeros(sel.size + 1, np.int64)
+        np.cumsum(lens, out=o[1:])
+        pair = np.repeat(np.arange(sel.size), lens)
+        k = np.arange(int(o[-1]), dtype=np.int64) - o[pair]
+        src = off[sel][pair] + end[sel][pair] - (k - reps[pair])
+        out = np.where(k < reps[pair], A, flat[np.clip(src, 0, max(flat.size - 1, 0))])
+        return out.astype(np.uint8), o
+
+    xq, xq_off = reversed_ext(fq, q_off, qe)
+    xr, xr_off = reversed_ext(fr, r_off, re_)
+    mat = np.full((A + 1, A + 1), -127, dtype=np.int64)
+    mat[:A, :A] = scheme.as_array()
+    mat[A, A] = 127
+    xs = ScoringScheme.from_array(mat, scheme.gap_open, scheme.gap_extend)
+    # pairs kernel for queries the warp kernels hold in 32 bits, the strip pipeline
+    # (one launch per pair) beyond
+    xql = np.diff(xq_off)
+    got = {"score": np.zeros(sel.size, np.int64), "ref_end": np.zeros(sel.size, np.int64),
+           "query_end": np.zeros(sel.size, np.int64)}
+    short = np.nonzero(xql <= 1024)[0]
+    if short.size:
+        lq, lr = xql[short], np.diff(xr_off)[short]
+        sq = np.concatenate([xq[xq_off[i]:xq_off[i + 1]] for i in short])
+        sr = np.concatenate([xr[xr_off[i]:xr_off[i + 1]] for i in short])
+        o = pairs_align(sq, np.concatenate([[0], np.cumsum(lq)]), sr,
+                        np.concatenate([[0], np.cumsum(lr)]), scheme=xs, width=width)
+        for key in got:
+            got[key][short] = o[key]
+    for i in np.nonzero(xql > 1024)[0]:
+        o = align_long(xq[xq_off[i]:xq_off[i + 1]], xr[xr_off[i]:xr_off[i + 1]], xs, width=width)
+        for key in got:
+            got[key][i] = o[key]
+    want = 127 * reps + sc[sel]
+    if not np.array_equal(got["score"].astype(np.int64), want):
+        bad = int(np.nonzero(got["score"] != want)[0][0])
+        raise ValueError(f"pair {int(sel[bad])}: no alignment from the end cell reaches the score")
+    rs[sel] = (re_[sel] - (got["ref_end"] - reps)).astype(np.int32)
+    qs[sel] = (qe[sel] - (got["query_end"] - reps)).astype(np.int32)
+    return rs, qs
+
+
 def batch_align(kernel_id, p, flat_q, q_off, flat_r, r_off, match_a, mis_a, go_a, ge_a):
     """src/_compiled.py:504-529: per-pair 4x4 DNA schemes, kernel_id 0 = lazy-F with
     early exit, 1 = lazy-F full, 2 = scan. Returns ``(scores int64[n], overflow

@@ -418,3 +418,29 @@ def merge_topk(records: torch.Tensor, k: int, group=None) -> torch.Tensor:
     key = (allr[:, 0] << 32) | (0xFFFFFFFF - (allr[:, 1] & 0xFFFFFFFF))
     _, idx = torch.topk(key, min(k, allr.shape[0]), sorted=True)
     return allr[idx].to(dev)
+
+
+def hit_starts(query, records, db: np.ndarray, offsets: np.ndarray, scheme: ScoringScheme,
+               width: int = 16) -> np.ndarray:
+    """Top-k hits with start coordinates: int64 [k, 6] (score, target_id, ref_end,
+    query_end, ref_start, query_start). ``records`` are topk/merge_topk records;
+    ``db``/``offsets`` the database CSR in global target ids. One device launch for
+    all hits (align.align_starts); hits without located ends keep (-1, -1)."""
+    from .align import align_starts
+
+    rec = records.cpu().numpy() if isinstance(records, torch.Tensor) else np.asarray(records)
+    rec = rec.astype(np.int64).reshape(-1, 4)
+    rec = rec[rec[:, 0] >= 0]
+    k = rec.shape[0]
+    q = np.asarray(query, dtype=np.uint8)
+    offsets = np.asarray(offsets, dtype=np.int64)
+    q_off = np.arange(k + 1, dtype=np.int64) * q.size
+    ids = rec[:, 1]
+    lens = offsets[ids + 1] - offsets[ids]
+    r_off = np.zeros(k + 1, np.int64)
+    np.cumsum(lens, out=r_off[1:])
+    flat_r = (np.concatenate([db[offsets[i]:offsets[i + 1]] for i in ids]) if k
+              else np.zeros(0, np.uint8))
+    rs, qs = align_starts(np.tile(q, k), q_off, flat_r, r_off, scheme, rec[:, 0], rec[:, 2],
+                          rec[:, 3], width=width)
+    return np.concatenate([rec, rs[:, None].astype(np.int64), qs[:, None].astype(np.int64)], axis=1)
