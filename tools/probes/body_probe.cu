@@ -1,0 +1,89 @@
+// Word-body formulations of the striped cell update, timed in isolation: 8 warps
+// per SM sub-partition pair (2 CTAs x 128 threads per SM, as the config-2 kernel),
+// L = 16 register-resident words per thread, S from a small register table.
+// Variants move add-max DPX ops (VIADDMNMX, one pipe) to VIADD.16x2 + VIMNMX
+// pairs (VIADD issues to another pipe; VIMNMX to either), see pipe_probe.cu.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o body_probe body_probe.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+constexpr int L = 16;
+template <int V>
+__global__ void __launch_bounds__(128, 2) body(uint32_t* out, int cols, uint32_t ngo, uint32_t nge) {
+  uint32_t H[L], E[L], NJ[L], Sx[4];
+#pragma unroll
+  for (int c = 0; c < L; ++c) { H[c] = 0; E[c] = 0; NJ[c] = (uint32_t)(-(c) & 0xffff) * 0x10001u; }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) Sx[k] = ((threadIdx.x * 5 + k * 3) % 9 - 4) & 0xffff;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) Sx[k] *= 0x10001u;
+  uint32_t carry = 0, cm = 0, w = 0;
+  for (int i = 0; i < cols; ++i) {
+    uint32_t vh = __byte_perm(w, 0, 0x1044);
+    uint32_t F = 0;
+    const int sh = i & 3;
+#pragma unroll
+    for (int c = 0; c < L; ++c) {
+      const uint32_t S = Sx[(c + sh) & 3];
+      uint32_t u;
+      const uint32_t t = __vadd2(vh, S);
+      if (V & 16) u = __vmaxs2(t, E[c]);
+      else if (V & 2) u = __vmaxs2(__vadd2(vh, S), E[c]);
+      else u = __viaddmax_s16x2(vh, S, E[c]);
+      const uint32_t Hn = __vmaxs2(u, F);
+      const uint32_t Xu = __vadd2(u, ngo);
+      if (V & 4) E[c] = __vimax_s16x2_relu(__vadd2(E[c], nge), Xu);
+      else E[c] = __viaddmax_s16x2_relu(E[c], nge, Xu);
+      F = __viaddmax_s16x2_relu(F, nge, Xu);
+      if (V & 16) cm = __vmaxs2(cm, t);
+      else if (V & 8) cm = __vimax3_s16x2(cm, u, cm);
+      else cm = __vmaxs2(cm, u);
+      if (V & 1) vh = __vmaxs2(__vadd2(carry, NJ[c]), H[c]);
+      else vh = __viaddmax_s16x2(carry, NJ[c], H[c]);
+      H[c] = Hn;
+    }
+    w = H[L - 1];
+    carry = __vmaxs2(F, carry) & 0x00ff00ffu;  // stands in for the per-column scan
+  }
+  uint32_t s = cm ^ carry;
+#pragma unroll
+  for (int c = 0; c < L; ++c) s ^= H[c] ^ E[c];
+  if (s == 0x9e3779b9u) out[threadIdx.x] = s;
+}
+
+template <int V>
+void run(uint32_t* d, int sms, const char* name) {
+  const int cols = 4000;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  body<V><<<sms * 2, 128>>>(d, 10, 0xfff5fff5u, 0xffffffffu);
+  cudaEventRecord(a);
+  body<V><<<sms * 2, 128>>>(d, cols, 0xfff5fff5u, 0xffffffffu);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  const double cells = (double)sms * 2 * 128 * cols * L * 2;
+  printf("variant %2d %-34s %8.3f ms  %7.1f GCUPS\n", V, name, ms, cells / (ms * 1e6));
+}
+
+int main() {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  uint32_t* d;
+  cudaMalloc(&d, 4096);
+  for (int rep = 0; rep < 2; ++rep) {
+    run<0>(d, sms, "current (4 VIADDMNMX)");
+    run<1>(d, sms, "vh split");
+    run<2>(d, sms, "u split");
+    run<4>(d, sms, "E split");
+    run<3>(d, sms, "vh+u split");
+    run<5>(d, sms, "vh+E split");
+    run<6>(d, sms, "u+E split");
+    run<8>(d, sms, "current, cm via VIMNMX3");
+    run<9>(d, sms, "vh split, cm via VIMNMX3");
+    run<16>(d, sms, "t = vh+S kept: u = max(t,E), cm over t");
+  }
+  return 0;
+}
