@@ -9,9 +9,14 @@
 #include <cuda_runtime.h>
 
 constexpr int L = 16;
+__device__ __forceinline__ uint32_t hmx(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("max.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
 template <int V>
 __global__ void __launch_bounds__(128, 2) body(uint32_t* out, int cols, uint32_t ngo, uint32_t nge) {
-  uint32_t H[L], E[L], NJ[L], Sx[4];
+  uint32_t H[L], E[L], NJ[L], Sx[4], Hp[L];
 #pragma unroll
   for (int c = 0; c < L; ++c) { H[c] = 0; E[c] = 0; NJ[c] = (uint32_t)(-(c) & 0xffff) * 0x10001u; }
 #pragma unroll
@@ -28,19 +33,27 @@ __global__ void __launch_bounds__(128, 2) body(uint32_t* out, int cols, uint32_t
       const uint32_t S = Sx[(c + sh) & 3];
       uint32_t u;
       const uint32_t t = __vadd2(vh, S);
-      if (V & 16) u = __vmaxs2(t, E[c]);
+      if ((V & 512) && c > 0) {
+        const uint32_t a = __vadd2(Hp[c - 1], S);
+        const uint32_t b = __vadd2(__vadd2(carry, NJ[c - 1]), S);
+        u = __vimax3_s16x2(a, b, E[c]);
+      } else if (V & 128) u = hmx(t, E[c]);
+      else if (V & 16) u = __vmaxs2(t, E[c]);
       else if (V & 2) u = __vmaxs2(__vadd2(vh, S), E[c]);
       else u = __viaddmax_s16x2(vh, S, E[c]);
-      const uint32_t Hn = __vmaxs2(u, F);
+      const uint32_t Hn = (V & 32) ? hmx(u, F) : __vmaxs2(u, F);
       const uint32_t Xu = __vadd2(u, ngo);
       if (V & 4) E[c] = __vimax_s16x2_relu(__vadd2(E[c], nge), Xu);
       else E[c] = __viaddmax_s16x2_relu(E[c], nge, Xu);
       F = __viaddmax_s16x2_relu(F, nge, Xu);
-      if (V & 16) cm = __vmaxs2(cm, t);
+      if (V & 32) cm = hmx(cm, u);
+      else if (V & 16) cm = __vmaxs2(cm, t);
       else if (V & 8) cm = __vimax3_s16x2(cm, u, cm);
       else cm = __vmaxs2(cm, u);
-      if (V & 1) vh = __vmaxs2(__vadd2(carry, NJ[c]), H[c]);
+      if (V & 64) vh = hmx(__vadd2(carry, NJ[c]), H[c]);
+      else if (V & 1) vh = __vmaxs2(__vadd2(carry, NJ[c]), H[c]);
       else vh = __viaddmax_s16x2(carry, NJ[c], H[c]);
+      if (V & 512) { Hp[c] = H[c]; }
       H[c] = Hn;
     }
     w = H[L - 1];
@@ -84,6 +97,12 @@ int main() {
     run<8>(d, sms, "current, cm via VIMNMX3");
     run<9>(d, sms, "vh split, cm via VIMNMX3");
     run<16>(d, sms, "t = vh+S kept: u = max(t,E), cm over t");
+    run<32>(d, sms, "Hn, cm via max.f16x2");
+    run<96>(d, sms, "Hn, cm, vh via max.f16x2");
+    run<160>(d, sms, "Hn, cm, u via max.f16x2");
+    run<36>(d, sms, "Hn, cm via f16x2, E split");
+    run<512>(d, sms, "u = max3(Hold+S, carry+NJ+S, E)");
+    run<520>(d, sms, "max3 u, cm via VIMNMX3");
   }
   return 0;
 }
