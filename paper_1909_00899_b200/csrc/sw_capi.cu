@@ -418,9 +418,14 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
   }
   // exact instances stage the profile as [sym][ceil(L/4)][T][4]
   // (T = 4: two copies at 32-word block granularity, see DUP in sw_kernels.cuh)
-  const size_t smem = block == 128 ? (size_t)(p->n_sym + 1) * ((p->seg_len + 3) / 4 * 4) * p->threads * 4 *
-                                         (p->threads == 4 ? 2 : 1)
-                                   : (size_t)p->prof_words * 4;
+  const size_t prof_bytes = block == 128 ? (size_t)(p->n_sym + 1) * ((p->seg_len + 3) / 4 * 4) * p->threads *
+                                               4 * (p->threads == 4 ? 2 : 1)
+                                         : (size_t)p->prof_words * 4;
+  // + the end-coordinate snapshots (SWB_SNAP): LMAX words per thread, only when
+  // coordinates are requested (score-only launches keep their occupancy)
+  const int lmax_k = block == 128 ? p->seg_len : p->lmax;
+  const bool snap = SWB_SNAP && (d_ref_end || d_query_end);
+  const size_t smem = (prof_bytes + 15) / 16 * 16 + (snap ? (size_t)block * (lmax_k | 1) * 4 : 0);
   const int G = 32 / p->threads;
   const int64_t tasks = d_n_jobs ? 0 : (n + G - 1) / G;
   return launch(fn, a, smem, block, tasks, (cudaStream_t)stream);
@@ -509,7 +514,11 @@ int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8
   a.pair_stride = (n_sym + 1) * lslice * p.threads;
   // block size: as many warps as the per-group profile slices allow (<= 256 threads)
   int block = max_block;
-  const size_t per_thread = (size_t)(n_sym + 1) * lslice * 4;  // slice bytes / T
+  // slice bytes / T, + the end-coordinate snapshot of the thread (SWB_SNAP)
+  const int lmax_k = vec ? p.seg_len : p.lmax;
+  const bool snap = SWB_SNAP && (d_ref_end || d_query_end);  // score-only: no snapshots
+  const size_t per_thread =
+      (size_t)(n_sym + 1) * lslice * 4 + (snap ? (size_t)(lmax_k | 1) * 4 : 0);
   while (block > 32 && per_thread * block > 110 * 1024) block >>= 1;
   const size_t smem = per_thread * block;
   if (smem > 227 * 1024) return fail(SW_ENOTSUP, "pair profile slice too large (%zu B)", smem);

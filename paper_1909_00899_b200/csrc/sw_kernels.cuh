@@ -362,8 +362,26 @@ sw_striped_kernel(const SwArgs a) {
 #endif
   // chunk of the running column maxima (a position search scans one chunk):
   // 16 words for the long exact segments (fewer maxima to combine per column)
+  // End coordinates: a thread whose column maximum beats the alignment's best so
+  // far stores the column's words (its snapshot) to shared memory -- LMAX
+  // STS.32 -- and the first word reaching the final best is located once, from
+  // the last snapshot, when the alignment ends (the best only grows, so the last
+  // snapshot holds the column of the final best). Searching in registers at every
+  // improvement (planted reads improve on most columns) cost the warp ~70 issue
+  // slots per improving column; SWB_SNAP=0 restores it (chunked column maxima).
+#ifndef SWB_SNAP
+#define SWB_SNAP 1
+#endif
+  constexpr bool SNAP = SWB_SNAP;
+  constexpr int SNW = LMAX | 1;  // snapshot words per thread (odd: rows spread over the banks)
+  // (chunked column maxima also with SNAP: independent accumulators, short chains)
   constexpr int kCh = SWB_KCH > 0 ? SWB_KCH : (EXACT && LMAX > 32 ? 16 : 8);
   constexpr int kNch = (LMAX + kCh - 1) / kCh;
+  // end-coordinate snapshots: SNW words per thread after the profile / the slices
+  const int prof_w = a.mode == 0 ? (VEC ? (A + 1) * LP4 * BW : (A + 1) * L * T)
+                                 : (int)(blockDim.x / T) * a.pair_stride;
+  uint32_t* const snap = smem + (prof_w + 3) / 4 * 4 + threadIdx.x * SNW;
+  (void)snap;
 
   // Task claiming: with a counter, warps take the next task (in length-descending
   // order) when they finish one -- longest-first greedy, so the warps end together
@@ -460,6 +478,7 @@ sw_striped_kernel(const SwArgs a) {
     // score-only launches (no coordinate outputs) never search: the gate never opens
     int gb = no_coords ? 0x7fffffff : floor_mode ? floor_v - 1 : 0;
     int bv = 0, bcol = -1, bq = -1;   // this thread's first-maximum record
+    int bh = 0;                       // SNAP: the half (lane) holding bv
     // running maxima of u per chunk of kCh words (never reset: a chunk reaches a
     // value above gb only in the column that first produces it)
     uint32_t cmk[kNch];
@@ -533,7 +552,21 @@ sw_striped_kernel(const SwArgs a) {
 #pragma unroll
       for (int k = 1; k < kNch; ++k) cm = Wd::vmax(cm, cmk[k]);
       const int cmx = Wd::hmax(cm);
-      if (cmx > gb) {
+      if (SNAP && cmx > gb) {
+        bool now = false;
+#pragma unroll
+        for (int h = 0; h < Wd::LPW; ++h) {
+          const int cv = Wd::get(cm, h);
+          if (cv > gb && cv > bv) { bv = cv; bcol = i; bh = h; now = true; }
+        }
+        if (now) {
+          // one STS.32 per word at immediate offsets (odd row stride: few bank
+          // conflicts); a 128-bit store would need H in aligned register quads,
+          // which costs ~45 moves per column
+#pragma unroll
+          for (int c = 0; c < LMAX; ++c) snap[c] = H[c];
+        }
+      } else if (!SNAP && cmx > gb) {
 #pragma unroll
         for (int h = 0; h < Wd::LPW; ++h) {
           const int cv = Wd::get(cm, h);
@@ -634,6 +667,13 @@ sw_striped_kernel(const SwArgs a) {
       }
     }
 
+    if (SNAP && bcol >= 0) {
+      // the first word of the snapshot column reaching bv (a diagonal cell: H == u)
+      int jj = LMAX - 1;
+      for (int c = LMAX - 1; c >= first; --c)
+        if (Wd::get(snap[c], bh) >= bv) jj = c;
+      bq = (bh * T + t) * L + (jj - first);
+    }
     // ---- reduce (best desc, ref_end asc, query_end asc) over the group ----
     int best = bv, col = bcol, q = bq;
     int sc;  // the score: the running maximum (equals best unless the floor skipped it)

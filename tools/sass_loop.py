@@ -1,8 +1,8 @@
 """Instruction histogram of the innermost loop containing a given SASS opcode.
 
 python tools/sass_loop.py <file.sass> [OPCODE]   (cuobjdump -sass -fun <kernel> output)
-Finds every backward branch whose range covers the first OPCODE instruction and
-prints the opcode counts of the smallest such range (the column loop).
+Picks the backward-branch range holding the most OPCODE instructions (the column
+loop) and prints its opcode counts.
 """
 import re
 import sys
@@ -15,16 +15,17 @@ for line in open(path):
     m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(@!?U?P\w+\s+)?([A-Z0-9_.]+)(.*?);", line)
     if m:
         ins.append((int(m.group(1), 16), m.group(3), m.group(4)))
-hot = next(a for a, op, _ in ins if op.startswith(key))
-best = None
+keys = [a for a, op, _ in ins if op.startswith(key)]
+rngs = []  # backward-branch ranges
 for a, op, rest in ins:
     if op.startswith("BRA"):
         t = re.search(r"0x([0-9a-f]+)", rest)
-        if t:
+        if t and int(t.group(1), 16) < a:
             tgt = int(t.group(1), 16)
-            if tgt <= hot <= a and (best is None or a - tgt < best[1] - best[0]):
-                best = (tgt, a)
-lo, hi = best
+            rngs.append((tgt, a, sum(tgt <= k <= a for k in keys)))
+top = max(n for _, _, n in rngs)
+# the smallest loop holding >= 90 % of the most OPCODE instructions any loop holds
+lo, hi, _ = min((r for r in rngs if r[2] >= 0.9 * top), key=lambda r: r[1] - r[0])
 c = Counter(op for a, op, _ in ins if lo <= a <= hi)
 print(f"loop 0x{lo:x}..0x{hi:x}: {sum(c.values())} instructions")
 for op, n in c.most_common():
