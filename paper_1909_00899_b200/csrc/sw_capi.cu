@@ -36,7 +36,7 @@ KernelTable g_tab[2][3];
 ExactTable g_exact;  // 16-bit scan, exact segment length
 const void* g_chain[2][6];  // strip pipeline [width][L = 1, 2, 4, 8, 16, 32]
 const void* g_chain_prof[2];
-const void* g_wave[4];
+const void* g_wave[4][4];  // [L = 1, 2, 4, 8][KC = 1, 2, 4, 8]
 const void* g_block[2][3][16];  // block / cluster scan [width][variant][L-1]  // strip pipeline, intra-strip wavefront [L = 1, 2, 4, 8]
 std::once_flag g_once;
 
@@ -531,6 +531,7 @@ int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8
 // total ~ (n + nb*K) * t(L); prefer the smallest total.
 struct ChainGeo {
   int li, L, nb;
+  int ki = 0, KC = 1;  // wavefront: columns per step (index into 1, 2, 4, 8)
   size_t prof_words, ring_bytes, total;
 };
 
@@ -598,8 +599,20 @@ static ChainGeo wave_geo(int64_t m, int64_t n, int n_sym) {
       g.li = li; g.L = L; g.nb = (int)(nb < 1 ? 1 : nb);
     }
   }
+  // Columns per step (tools/wave_sweep.py, B200): two columns per step at one row
+  // per lane win while the 1-row strips fit one warp per SM sub-partition (config 1
+  // 0.52 -> 0.38 ms, config 4 5.0 -> 3.7 ms); beyond that taller strips at one
+  // column per step do (config 5: L = 4, KC = 1, 62 ms; KC = 2 / 4: 79 / 64 ms).
+  int kc = 1;
+  if (!force && (m + 31) / 32 <= 148 * 4) {
+    g.li = 0; g.L = 1; g.nb = (int)((m + 31) / 32);
+    kc = 2;
+  }
+  if (const char* f = getenv("SWB_WAVE_KC")) kc = atoi(f);
+  g.ki = kc >= 8 ? 3 : kc >= 4 ? 2 : kc >= 2 ? 1 : 0;
+  g.KC = 1 << g.ki;
   g.prof_words = (size_t)g.nb * (n_sym + 1) * g.L * 32;
-  g.ring_bytes = (size_t)g.nb * kChainRing * kChainK * sizeof(int2);
+  g.ring_bytes = (size_t)g.nb * kChainRing * kChainK * g.KC * sizeof(int2);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   g.total = al(g.prof_words * 4) + al(g.ring_bytes) + al(g.nb * 128) * 2 + al(g.nb * 16) + 256;
   return g;
@@ -689,8 +702,8 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
     a.trace_tiles = atoi(getenv("SWB_CHAIN_TRACE_TILES"));
     a.reverse = getenv("SWB_CHAIN_REVERSE") != nullptr;
   }
-  const void* fn = wave ? g_wave[g.li] : g_chain[wi][g.li];
-  const size_t smem = wave ? (size_t)(n_sym + 1) * g.L * 32 * 4 + 128 + 3 * kChainK * 8  // residues, tile_in, 2 x tile_out
+  const void* fn = wave ? g_wave[g.li][g.ki] : g_chain[wi][g.li];
+  const size_t smem = wave ? (size_t)(n_sym + 1) * g.L * 32 * 4 + 128 * g.KC + 3 * kChainK * g.KC * 8  // residues, tile_in, 2 x tile_out
                            : (size_t)(n_sym + 1) * g.L * 32 * 4 + kChainK * (16 + 8);  // + tile staging
   if (smem > 48 * 1024) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -869,6 +869,6 @@ SWB_X_DECL(16, 0, c) SWB_X_DECL(16, 1, c) SWB_X_DECL(16, 2, c)
 SWB_X_DECL(32, 0, c) SWB_X_DECL(32, 1, c) SWB_X_DECL(32, 2, c)
 #undef SWB_X_DECL
 void swb_fill_chain(const void* (&tab)[2][6], const void* (&ptab)[2]);
-void swb_fill_wave(const void* (&tab)[4]);
+void swb_fill_wave(const void* (&tab)[4][4]);
 void swb_fill_block16(const void* (&tab)[3][16]);
 void swb_fill_block32(const void* (&tab)[3][16]);

@@ -530,14 +530,17 @@ def test_long_pair_pipeline_random(A, oracle):
         assert (got["score"], got["ref_end"], got["query_end"]) == want, (trial, "wave", m, n)
 
 
+@pytest.mark.parametrize("cols_per_step", [1, 2, 4, 8])
 @pytest.mark.parametrize("rows_per_lane", [1, 2, 4, 8])
-def test_wavefront_strip_heights(A, oracle, rows_per_lane, monkeypatch):
-    """Every wavefront strip height (forced), ragged last strips, n < 32, planted and
-    random pairs, against the scalar oracle."""
+def test_wavefront_strip_heights(A, oracle, rows_per_lane, cols_per_step, monkeypatch):
+    """Every wavefront tile shape (forced rows per lane x columns per step), ragged
+    last strips and super-columns, n < 32, planted and random pairs, against the
+    scalar oracle."""
     from paper_1909_00899_b200.scoring import ScoringScheme
 
     monkeypatch.setenv("SWB_WAVE_L", str(rows_per_lane))
-    rng = np.random.default_rng(0x3A7E + rows_per_lane)
+    monkeypatch.setenv("SWB_WAVE_KC", str(cols_per_step))
+    rng = np.random.default_rng(0x3A7E + rows_per_lane + 16 * cols_per_step)
     for trial in range(6):
         k = int(rng.integers(2, 21))
         mat = rng.integers(-5, 6, (k, k))
