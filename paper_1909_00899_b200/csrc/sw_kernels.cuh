@@ -241,6 +241,9 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #ifndef SWB_EXACT_MINB
 #define SWB_EXACT_MINB 3  // CTAs of 128 threads per SM the exact kernels are register-capped for
 #endif
+#ifndef SWB_EXACT_LONG_MINB
+#define SWB_EXACT_LONG_MINB 2  // the same for segments over 32 words
+#endif
 #ifndef SWB_COL_UNROLL
 #define SWB_COL_UNROLL 1  // reference columns per loop iteration (unroll factor)
 #endif
@@ -248,7 +251,7 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #define SWB_UNROLL(n) SWB_PRAGMA(unroll n)
 
 template <class Wd, int T, int LMAX, int VAR, bool EXACT = false, int GE = 0>
-__global__ void __launch_bounds__(EXACT ? 128 : 256, EXACT ? (LMAX > 32 ? 2 : SWB_EXACT_MINB) : 1)
+__global__ void __launch_bounds__(EXACT ? 128 : 256, EXACT ? (LMAX > 32 ? SWB_EXACT_LONG_MINB : SWB_EXACT_MINB) : 1)
 sw_striped_kernel(const SwArgs a) {
   // GE > 0: gap-extend penalty known at compile time, so every decay constant
   // (j*ge, k*L*ge) is an immediate operand of VIADDMNMX instead of a register.
@@ -295,8 +298,11 @@ sw_striped_kernel(const SwArgs a) {
   uint32_t NKD[STEPS];
   int bias = a.bias, max_sub = a.max_sub;
 
-  auto set_gaps = [&](int go, int ge_rt, int L_) {
+  auto set_gaps = [&](int go, int ge_rt, int L_rt) {
     const int ge = GE > 0 ? GE : ge_rt;
+    // exact instances: the segment length is LMAX (host-guaranteed), so with a
+    // compile-time ge every decay is an immediate operand, not a register
+    const int L_ = EXACT ? LMAX : L_rt;
     const int cl = Wd::CLAMP;
     NGO = Wd::splat(-min(go, cl));
     NGE = Wd::splat(-min(ge, cl));
@@ -315,7 +321,7 @@ sw_striped_kernel(const SwArgs a) {
   int LT;                     // words per profile row
   if (a.mode == 0) {
     // DB mode: one profile for the whole launch, staged in shared memory.
-    L = a.shared_L;
+    L = EXACT ? LMAX : a.shared_L;
     m = a.shared_m;
     first = LMAX - L;
     LT = L * T;

@@ -7,5 +7,5 @@ for so in "" vt/*/libswscan_b200.so; do
   echo "== ${so:-in-tree}"
   if [ -n "$so" ]; then export SWB_LIB_PATH=$PWD/$so; else unset SWB_LIB_PATH; fi
   python tools/prof_db.py --n-targets 1000000 --reps 3 --floor-topk 100 | tail -2
-  python tools/bench_configs.py --configs 3 --c3-pairs 16777216 --reps 3 | grep -v lazyf
+  python tools/bench_configs.py --configs 3 --c3-pairs 16777216 --reps 3 | grep -v lazyf | cut -c1-140
 done
