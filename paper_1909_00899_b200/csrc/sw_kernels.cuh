@@ -244,6 +244,9 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #ifndef SWB_EXACT_LONG_MINB
 #define SWB_EXACT_LONG_MINB 2  // the same for segments over 32 words
 #endif
+#ifndef SWB_OWN_GATE
+#define SWB_OWN_GATE 1
+#endif
 #ifndef SWB_COL_UNROLL
 #define SWB_COL_UNROLL 1  // reference columns per loop iteration (unroll factor)
 #endif
@@ -480,7 +483,10 @@ sw_striped_kernel(const SwArgs a) {
       if (lane == 0) floor_v = *(volatile const int32_t*)a.coord_floor;
       floor_v = __shfl_sync(0xffffffffu, floor_v, 0);
     }
-    const bool floor_mode = floor_v > 0;
+    // per-thread gate (own best): no group reduction per column; with snapshots a
+    // thread records its own first maximum and the group reduction at the end
+    // picks the alignment's (SWB_OWN_GATE)
+    const bool floor_mode = floor_v > 0 || (SNAP && SWB_OWN_GATE);
     // score-only launches (no coordinate outputs) never search: the gate never opens
     int gb = no_coords ? 0x7fffffff : floor_mode ? floor_v - 1 : 0;
     int bv = 0, bcol = -1, bq = -1;   // this thread's first-maximum record
