@@ -95,7 +95,7 @@ class ClockSampler:
                     rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 except AttributeError:
                     rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                self.rows.append((float(sm), float(mx), int(rs)))
+                self.rows.append((float(sm), float(mx), int(rs), time.perf_counter()))
             except Exception:
                 pass
             time.sleep(0.005)
@@ -105,17 +105,25 @@ class ClockSampler:
             self.thread = threading.Thread(target=self._loop, daemon=True)
             self.thread.start()
 
+    def mark(self) -> None:
+        """Start of the timed region (the sampler runs from before the warm-up, so
+        NVML's first, slow calls are out of the way by then)."""
+        self.t0 = time.perf_counter()
+
     def stop(self) -> dict:
         if self.thread is None:
             return self._smi()
+        t1 = time.perf_counter()
         self._stop.set()
         self.thread.join(timeout=2)
-        sm = [r[0] for r in self.rows]
-        reasons = sorted({name for r in self.rows for bit, name in self.REASONS.items()
+        t0 = getattr(self, "t0", 0.0)
+        rows = [r for r in self.rows if t0 <= r[3] <= t1] or self.rows[-3:]
+        sm = [r[0] for r in rows]
+        reasons = sorted({name for r in rows for bit, name in self.REASONS.items()
                           if r[2] & bit})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(r[1] for r in self.rows) if self.rows else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "sm_max_mhz": max(r[1] for r in rows) if rows else None,
+                "reasons": reasons, "samples": len(rows)}
 
     def _smi(self) -> dict:
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -261,14 +269,15 @@ def main() -> None:
         top = eng.topk(TOPK)
         return search.merge_topk(top, TOPK)
 
+    sampler = ClockSampler(local)
+    sampler.start()
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
 
     # ---- value: device-resident inputs, whole step, max over ranks ----
     launches0 = eng.launches
-    sampler = ClockSampler(local)
-    sampler.start()
+    sampler.mark()
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
