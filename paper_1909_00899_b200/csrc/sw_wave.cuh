@@ -52,7 +52,8 @@ __device__ __forceinline__ void wave_step(WaveLane<L, KC>& w, const int s, const
                                           const int n, const int A, const uint8_t* sref,
                                           const uint32_t* sprof, const int2* tile_in,
                                           int2* tlo, int2* thi, const bool handoff,
-                                          const uint32_t NGO, const uint32_t NGE, const int qbase) {
+                                          const uint32_t NGO, const uint32_t NGE, const int qbase,
+                                          const uint32_t (&NJG)[L + 1]) {
   using Wd = W32;
   constexpr int RMASK = 128 * KC - 1;  // residue ring: 4 handoff tiles of columns
   const int B = s - lane;
@@ -93,20 +94,47 @@ __device__ __forceinline__ void wave_step(WaveLane<L, KC>& w, const int s, const
   uint32_t um[KC][L];
 #pragma unroll
   for (int r = 0; r < KC; ++r) {
-    uint32_t diag = r == 0 ? w.hab_prev : up_h[r - 1];
-    uint32_t F = fin[r];
+    if constexpr (L <= 2) {  // short lanes: the plain F chain (fewer instructions)
+      uint32_t diag = r == 0 ? w.hab_prev : up_h[r - 1];
+      uint32_t F = fin[r];
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        const uint32_t u = Wd::addmax(diag, S[r][j], w.E[j]);
+        diag = w.H[j];
+        const uint32_t Xu = Wd::add(u, NGO);
+        w.E[j] = Wd::addmax_relu(w.E[j], NGE, Xu);
+        w.H[j] = Wd::vmax(u, F);
+        F = Wd::addmax_relu(F, NGE, Xu);
+        um[r][j] = u;
+      }
+      w.h_bot[r] = w.H[L - 1];
+      w.f_bot[r] = F;
+      continue;
+    }
+    // Everything but the incoming F first: u, E and the lane-local F prefix
+    // B_j = max(B_{j-1} - ge, Xu_j, 0) do not depend on the lane above, so they
+    // overlap the shuffle; then F_j = max(F_in - j*ge, B_{j-1}) is one op per row
+    // and the lane-to-lane path per step is the shuffle plus two DPX ops (instead
+    // of the shuffle plus an L-long F chain; config 5 at L = 8: 154 -> 100 ms).
+    uint32_t B[L];
 #pragma unroll
     for (int j = 0; j < L; ++j) {
+      const uint32_t diag = j == 0 ? (r == 0 ? w.hab_prev : up_h[r - 1]) : w.H[j - 1];
       const uint32_t u = Wd::addmax(diag, S[r][j], w.E[j]);
-      diag = w.H[j];
-      const uint32_t Xu = Wd::add(u, NGO);
-      w.E[j] = Wd::addmax_relu(w.E[j], NGE, Xu);
-      w.H[j] = Wd::vmax(u, F);
-      F = Wd::addmax_relu(F, NGE, Xu);
       um[r][j] = u;
     }
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      const uint32_t Xu = Wd::add(um[r][j], NGO);
+      w.E[j] = Wd::addmax_relu(w.E[j], NGE, Xu);
+      B[j] = j == 0 ? Wd::addmax_relu(Xu, 0u, 0u) : Wd::addmax_relu(B[j - 1], NGE, Xu);
+    }
+    const uint32_t F = fin[r];
+#pragma unroll
+    for (int j = 0; j < L; ++j)
+      w.H[j] = Wd::vmax(um[r][j], j == 0 ? F : Wd::addmax(F, NJG[j], B[j - 1]));
     w.h_bot[r] = w.H[L - 1];
-    w.f_bot[r] = F;
+    w.f_bot[r] = Wd::addmax(F, NJG[L], B[L - 1]);
   }
   w.hab_prev = up_h[KC - 1];
   // first maximum of this lane (a best cell is a diagonal cell, observed as u): the
@@ -187,6 +215,9 @@ __global__ void __launch_bounds__(32) sw_wave_kernel(const ChainArgs a) {
 
   const int cl = W32::CLAMP;
   const uint32_t NGO = (uint32_t)-min(a.go, cl), NGE = (uint32_t)-min(a.ge, cl);
+  uint32_t NJG[L + 1];  // -j * ge (clamped): decay of the incoming F at row j
+#pragma unroll
+  for (int j = 0; j <= L; ++j) NJG[j] = (uint32_t)-(int)min((int64_t)j * a.ge, (int64_t)cl);
   WaveLane<L, KC> w;
 #pragma unroll
   for (int j = 0; j < L; ++j) { w.H[j] = 0u; w.E[j] = 0u; }
@@ -313,13 +344,13 @@ __global__ void __launch_bounds__(32) sw_wave_kernel(const ChainArgs a) {
 #pragma unroll (UNR)
       for (int k = 0; k < TS; ++k)
         wave_step<L, KC, false>(w, t0 + k, k, lane, n, A, sref, sprof, tile_in, tlo, thi, handoff,
-                                NGO, NGE, qbase);
+                                NGO, NGE, qbase, NJG);
     } else {
 #pragma unroll (UNR)
       for (int k = 0; k < TS; ++k)
         if (t0 + k < steps)
           wave_step<L, KC, true>(w, t0 + k, k, lane, n, A, sref, sprof, tile_in, tlo, thi, handoff,
-                                 NGO, NGE, qbase);
+                                 NGO, NGE, qbase, NJG);
     }
   }
   // the last (partial) outgoing tiles
