@@ -34,7 +34,10 @@ namespace swb {
 #define SWB_CHAIN_BP_ALL 1
 #endif
 constexpr int kChainK = 32;     // columns per handoff tile
-constexpr int kChainRing = 8;   // tiles in flight per boundary
+#ifndef SWB_CHAIN_RING
+#define SWB_CHAIN_RING 32  // tiles per boundary ring (8 -> 32: config 5 wavefront 62.7 -> 59.4 ms, scan 196 -> 192 ms)
+#endif
+constexpr int kChainRing = SWB_CHAIN_RING;  // tiles in flight per boundary
 
 struct ChainArgs {
   const uint32_t* prof;   // [(A+1)][L][32] words, striped per strip (see sw_chain_profile_kernel)
