@@ -396,8 +396,8 @@ def main() -> None:
                          "peak": round(peak_gcups, 2), "unit": "GCUPS",
                          "frac": round(kernel_gcups / peak_gcups, 4),
                          # dram__bytes_read+write per launch of this kernel (one ncu --set
-                         # full capture at this config, profiles/r01h_config2_db_kernel.md)
-                         "traffic": 513.44e6,
+                         # full capture at this config, profiles/r01i_config2_db_kernel.md)
+                         "traffic": 509.05e6,
                          "kernel": (f"sw_striped_kernel<W16,T={eng.plan16.threads},"
                                     f"L={eng.plan16.seg_len},{args.kernel.upper()},ge={w.scheme.gap_extend}>"),
                          "kernel_ms": round(k_ms, 3),
