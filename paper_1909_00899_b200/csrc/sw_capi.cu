@@ -374,7 +374,7 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
   if (wi == 0 && var == VAR_SCAN) {
     const int gi = (gap_extend == 1 || gap_extend == 2) ? gap_extend : 0;
     fn = g_exact[gi][ilog2(p->threads)][p->seg_len];
-    if (fn) block = 128;
+    if (fn) block = p->seg_len > 32 ? SWB_EXACT_LONG_BLOCK : 128;
   }
   if (!fn && li >= 0) fn = g_tab[wi][var][ilog2(p->threads)][li];
   if (!fn) return fail(SW_ENOTSUP, "no kernel for width %d, threads %d", p->width, p->threads);
@@ -418,12 +418,12 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
   }
   // exact instances stage the profile as [sym][ceil(L/4)][T][4]
   // (T = 4: two copies at 32-word block granularity, see DUP in sw_kernels.cuh)
-  const size_t prof_bytes = block == 128 ? (size_t)(p->n_sym + 1) * ((p->seg_len + 3) / 4 * 4) * p->threads *
+  const size_t prof_bytes = block != 256 ? (size_t)(p->n_sym + 1) * ((p->seg_len + 3) / 4 * 4) * p->threads *
                                                4 * (p->threads == 4 ? 2 : 1)
                                          : (size_t)p->prof_words * 4;
   // + the end-coordinate snapshots (SWB_SNAP): LMAX words per thread, only when
   // coordinates are requested (score-only launches keep their occupancy)
-  const int lmax_k = block == 128 ? p->seg_len : p->lmax;
+  const int lmax_k = block != 256 ? p->seg_len : p->lmax;
   const bool snap = SWB_SNAP && (d_ref_end || d_query_end);
   const size_t smem = (prof_bytes + 15) / 16 * 16 + (snap ? (size_t)block * (lmax_k | 1) * 4 : 0);
   const int G = 32 / p->threads;

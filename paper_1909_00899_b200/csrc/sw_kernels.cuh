@@ -241,6 +241,9 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #ifndef SWB_EXACT_MINB
 #define SWB_EXACT_MINB 3  // CTAs of 128 threads per SM the exact kernels are register-capped for
 #endif
+#ifndef SWB_EXACT_LONG_BLOCK
+#define SWB_EXACT_LONG_BLOCK 128  // threads per CTA of the database kernels over 32 words
+#endif
 #ifndef SWB_EXACT_LONG_MINB
 #define SWB_EXACT_LONG_MINB 2  // the same for segments over 32 words
 #endif
@@ -254,7 +257,8 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #define SWB_UNROLL(n) SWB_PRAGMA(unroll n)
 
 template <class Wd, int T, int LMAX, int VAR, bool EXACT = false, int GE = 0>
-__global__ void __launch_bounds__(EXACT ? 128 : 256, EXACT ? (LMAX > 32 ? SWB_EXACT_LONG_MINB : SWB_EXACT_MINB) : 1)
+__global__ void __launch_bounds__(EXACT ? (LMAX > 32 ? SWB_EXACT_LONG_BLOCK : 128) : 256,
+                                  EXACT ? (LMAX > 32 ? SWB_EXACT_LONG_MINB : SWB_EXACT_MINB) : 1)
 sw_striped_kernel(const SwArgs a) {
   // GE > 0: gap-extend penalty known at compile time, so every decay constant
   // (j*ge, k*L*ge) is an immediate operand of VIADDMNMX instead of a register.
