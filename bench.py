@@ -338,7 +338,11 @@ def main() -> None:
     peak_gcups = dpx_instr_per_s * 2 / 6 / 1e9
 
     # ---- e2e: public API with host buffers (H2D of the shard + D2H of the top-k) ----
-    h2d = packed.nbytes() + m
+    # what search_streamed copies per step: residues, starts, lengths, ids (the
+    # processing order is the identity for a length-sorted pack and stays on the
+    # device) + the query
+    h2d = sum(int(t.numel() * t.element_size())
+              for t in (packed.codes, packed.start, packed.length, packed.ids)) + m
     d2h = TOPK * 4 * 8
 
     # under a profiler (ncu injects itself through CUDA_INJECTION64_PATH) kernels are

@@ -84,8 +84,9 @@ int32_t sw_profile_build(const sw_plan_t* plan, const uint8_t* d_query, const in
  * applied to every target.  Targets: d_tgt bytes, target j = d_tgt[d_start[j] ..
  * d_start[j] + d_len[j]).  d_order (nullable): processing order of job ids
  * (length-sorted, descending, for load balance).  d_n_jobs (nullable): device
- * job count overriding n: a rescue pass that runs without a host sync; its
- * results are marked SW_FLAG_RESCUED.
+ * job count overriding n: a re-run pass that runs without a host sync (the
+ * 32-bit overflow rescue, whose results are marked SW_FLAG_RESCUED, or a 16-bit
+ * re-run of jobs whose streamed input timed out).
  * Outputs are indexed by job id; d_ref_end/d_query_end/d_flags/d_col_passes/d_pass_stats
  * nullable.  d_col_passes (lazy-F kernels): per-column correction passes of job 0.
  * d_pass_stats (lazy-F kernels): int64 [n][2] = (total correction passes, columns that
@@ -109,11 +110,16 @@ typedef struct sw_db_opts {
    * its jobs has arrived: jobs [c * arrive_jobs, (c + 1) * arrive_jobs) (ids before
    * d_order) are readable once d_arrived[c] >= arrive_epoch.  The caller copies
    * chunk c (residues, starts, lengths) and then the flag on one copy stream, so
-   * one launch overlaps the whole host-to-device transfer.  A chunk that never
-   * arrives (~17 s) marks its jobs SW_FLAG_FEED_TIMEOUT instead of hanging. */
+   * one launch overlaps the whole host-to-device transfer.  A task whose chunk
+   * has not arrived after arrive_timeout_ns (0 = 2 s) aborts the feed: it and every
+   * job not yet started report score 0 with SW_FLAG_FEED_TIMEOUT (no hang, no
+   * unflagged result).  The caller re-runs the flagged jobs once its copies are
+   * done (sw_collect_flagged(mask = SW_FLAG_FEED_TIMEOUT) + a device-counted
+   * sw_db_align); the Python layer does this in search_streamed. */
   int32_t arrive_epoch;
   const int32_t* d_arrived;
   int64_t arrive_jobs;
+  int64_t arrive_timeout_ns;
 } sw_db_opts_t;
 
 int32_t sw_db_align(const sw_plan_t* plan, const uint32_t* d_prof, int32_t kernel,

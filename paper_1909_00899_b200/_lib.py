@@ -23,7 +23,7 @@ KERNEL_IDS = {  # reference _KERNEL_IDS (src/_compiled.py:576) + parity-mode laz
     "lazyf-noexit-mirror": 4,
     "wavefront": 5,  # sw_align_long only: strip pipeline with an intra-strip wavefront
 }
-FLAG_REF_OVERFLOW, FLAG_RESCUE, FLAG_RESCUED = 1, 2, 4
+FLAG_REF_OVERFLOW, FLAG_RESCUE, FLAG_RESCUED, FLAG_FEED_TIMEOUT = 1, 2, 4, 8
 
 EXPORTS = (
     "sw_version",
@@ -62,6 +62,7 @@ class DbOpts(C.Structure):
         ("arrive_epoch", C.c_int32),
         ("d_arrived", C.c_void_p),
         ("arrive_jobs", C.c_int64),
+        ("arrive_timeout_ns", C.c_int64),
     ]
 
 

@@ -151,6 +151,19 @@ class DeviceProfile:
     long32: bool = False  # no 32-bit warp-kernel plan: rescues use the strip pipeline
     extra: dict = field(default_factory=dict)
 
+    # The reference returns a (prof, bias) tuple and its callers unpack it
+    # (`prof, bias = build_profile_arrays(...)`, src/runner.py:146,
+    # src/_compiled.py:614): a DeviceProfile unpacks as (itself, bias), so
+    # align_prebuilt(kernel, prof, bias, ref, scheme) works unchanged.
+    def __iter__(self):
+        return iter((self, self.bias))
+
+    def __len__(self) -> int:
+        return 2
+
+    def __getitem__(self, i: int):
+        return (self, self.bias)[i]
+
     @property
     def seg_len(self) -> int:
         return self.plan16.seg_len
@@ -205,9 +218,20 @@ def _plan_with_fallback(m: int, n_sym: int, width: int, lanes: int) -> _lib.Plan
     return _lib.plan_query(m, n_sym, width, 0)
 
 
+def as_scheme(scheme) -> ScoringScheme:
+    """Accept the reference's own ScoringScheme (src/scoring.py:56-98) or any object
+    with its fields (matrix, gap_open, gap_extend), so reference callers can pass
+    theirs unchanged; validation is the reference's (ValueError)."""
+    if isinstance(scheme, ScoringScheme):
+        return scheme
+    return ScoringScheme(scheme.matrix, scheme.gap_open, scheme.gap_extend)
+
+
 def build_profile_arrays(query, scheme: ScoringScheme, p: int = 0) -> DeviceProfile:
-    """Build the striped profile on the device (src/_compiled.py:579-585)."""
+    """Build the striped profile on the device (src/_compiled.py:579-585).
+    Unpacks as ``(prof, bias)`` like the reference's tuple."""
     _require_cuda()
+    scheme = as_scheme(scheme)
     q = _codes(query, scheme.n_symbols, "query")
     if q.size == 0:
         raise EmptyQuery("query must contain at least one residue")

@@ -8,7 +8,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "sw_chain.cuh"
 #include "sw_block.cuh"
@@ -184,32 +186,37 @@ int plan(int m, int n_sym, int width, int lanes, sw_plan_t* out) {
   return SW_OK;
 }
 
-// Task counters for dynamic task claiming (SwArgs::task_ctr) and the coordinate-floor
-// sample histogram: one slot = a 128-byte counter line + kFloorBins words, kCtrSlots
-// slots per device allocated once (~1 MB); each launch takes the next slot and zeroes
-// what it uses on its stream, so launches on different streams do not share a slot.
-constexpr int kCtrSlots = 64;
+// Task counters for dynamic task claiming (SwArgs::task_ctr: [0] task claims,
+// [1] sample tasks done, [2] streamed-input abort word) and the coordinate-floor
+// sample histogram: one slot = a 128-byte counter line + kFloorBins words.  Every
+// (device, stream) pair owns its own slot, allocated on first use: launches on one
+// stream run in order (each zeroes the slot on that stream before it runs), and
+// launches on different streams never share a slot, however many are in flight.
+// (A stream handle that is destroyed and re-created while its last launch still
+// runs would share the slot; destroy streams only after their work completed.)
 constexpr size_t kSlotBytes = 128 + kFloorBins * 4;
-constexpr int kMaxDev = 64;
+constexpr int64_t kDefaultArriveTimeoutNs = 2000000000ll;  // 2 s per chunk wait
 std::mutex g_ctr_mu;
-unsigned long long* g_ctr[kMaxDev] = {};
-std::atomic<uint32_t> g_ctr_next{0};
+std::map<std::pair<int, cudaStream_t>, char*> g_ctr_slots;
 
 cudaError_t task_counter(cudaStream_t stream, bool hist, unsigned long long** out,
                          uint32_t** hist_out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+  char* slot = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_ctr_mu);
-    if (!g_ctr[dev]) {
-      e = cudaMalloc((void**)&g_ctr[dev], (size_t)kCtrSlots * kSlotBytes);
+    auto it = g_ctr_slots.find({dev, stream});
+    if (it == g_ctr_slots.end()) {
+      e = cudaMalloc((void**)&slot, kSlotBytes);
       if (e != cudaSuccess) return e;
+      g_ctr_slots[{dev, stream}] = slot;
+    } else {
+      slot = it->second;
     }
   }
-  char* slot = (char*)g_ctr[dev] + (size_t)(g_ctr_next++ % kCtrSlots) * kSlotBytes;
-  e = cudaMemsetAsync(slot, 0, hist ? kSlotBytes : 2 * sizeof(unsigned long long), stream);
+  e = cudaMemsetAsync(slot, 0, hist ? kSlotBytes : 128, stream);
   *out = (unsigned long long*)slot;
   *hist_out = (uint32_t*)(slot + 128);
   return e;
@@ -414,6 +421,8 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
       a.arrived = opts->d_arrived;
       a.arrive_jobs = opts->arrive_jobs;
       a.arrive_epoch = opts->arrive_epoch;
+      a.arrive_timeout_ns =
+          opts->arrive_timeout_ns > 0 ? opts->arrive_timeout_ns : kDefaultArriveTimeoutNs;
     }
   }
   // exact instances stage the profile as [sym][ceil(L/4)][T][4]

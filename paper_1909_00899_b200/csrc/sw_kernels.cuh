@@ -59,6 +59,12 @@ __device__ __forceinline__ int ld_acquire_s32(const int32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
@@ -229,6 +235,7 @@ struct SwArgs {
   const int32_t* arrived;     // streamed input: chunk c readable once arrived[c] >= epoch
   int64_t arrive_jobs;        // jobs per chunk
   int32_t arrive_epoch;
+  int64_t arrive_timeout_ns;  // a chunk later than this aborts the feed (FLAG_FEED_TIMEOUT)
 };
 constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095 share the top bin)
 
@@ -419,13 +426,27 @@ sw_striped_kernel(const SwArgs a) {
     // chunk arrived can be reused.
     // (every lane waits for its own job's chunk: no warp collective here, which
     // would raise the register allocation of the whole kernel)
+    // A chunk that has not arrived after arrive_timeout_ns (globaltimer) -- e.g. the
+    // copy engine never ran concurrently with this kernel (profilers, serialised
+    // launches) -- raises the launch's abort word (task_ctr[2]); every waiting or
+    // later task then gives up at once and reports FLAG_FEED_TIMEOUT, and the host
+    // re-runs exactly those jobs once the copies are done (search_streamed): the
+    // feed can be slow, never wrong.
     bool feed_ok = true;
     if (a.arrived && valid) {
       const int32_t* flag = a.arrived + job / a.arrive_jobs;
-      unsigned spins = 0;
-      while (ld_acquire_s32(flag) < a.arrive_epoch) {
-        __nanosleep(256);
-        if (++spins == (1u << 26)) { feed_ok = false; break; }
+      if (ld_acquire_s32(flag) < a.arrive_epoch) {
+        volatile unsigned long long* abort_w = a.task_ctr + 2;
+        const uint64_t t0 = globaltimer_ns();
+        while (ld_acquire_s32(flag) < a.arrive_epoch) {
+          __nanosleep(512);
+          if (*abort_w != 0ull) { feed_ok = false; break; }
+          if (globaltimer_ns() - t0 > (uint64_t)a.arrive_timeout_ns) {
+            atomicExch(a.task_ctr + 2, 1ull);
+            feed_ok = false;
+            break;
+          }
+        }
       }
     }
     const int len = (valid && feed_ok) ? __ldcg(a.t_len + job) : 0;
@@ -715,7 +736,9 @@ sw_striped_kernel(const SwArgs a) {
         if (sc >= 32767 - max_sub) fl |= FLAG_RESCUE;
       }
       if (sc > 65535 - bias) fl |= FLAG_REF_OVERFLOW;
-      if (a.n_jobs_dev) fl |= FLAG_RESCUED;  // device-counted launches are rescue passes
+      // device-counted 32-bit launches are the overflow rescue passes (a 16-bit
+      // device-counted launch re-runs jobs whose streamed input timed out)
+      if (a.n_jobs_dev && Wd::LPW == 1) fl |= FLAG_RESCUED;
       if (!feed_ok) fl |= FLAG_FEED_TIMEOUT;
       if (sc == 0) { col = -1; q = -1; }
       else if (best != sc) { col = -2; q = -2; }  // below the coordinate floor: not located

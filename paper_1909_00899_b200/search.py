@@ -23,6 +23,7 @@ Top-k order: score descending, then global target id ascending.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -180,6 +181,9 @@ class DatabaseSearch:
         self.out: dict | None = None
         self.prof: DeviceProfile | None = None
         self.launches = 0
+        # streamed input: a chunk later than this aborts the feed and the jobs it
+        # held are re-run after the copies (0 = the library default, 2 s)
+        self.feed_timeout_ns = int(float(os.environ.get("SWB_FEED_TIMEOUT_MS", "0")) * 1e6)
 
     def _ensure_buffers(self, packed: PackedDb) -> None:
         n = packed.n
@@ -193,6 +197,8 @@ class DatabaseSearch:
                 "query_end": torch.empty(n, dtype=torch.int32, device="cuda"),
                 "flags": torch.empty(n, dtype=torch.uint8, device="cuda"),
                 "_rescue": (torch.empty(max(n, 1), dtype=torch.int32, device="cuda"),
+                            torch.zeros(1, dtype=torch.int64, device="cuda")),
+                "_refeed": (torch.empty(max(n, 1), dtype=torch.int32, device="cuda"),
                             torch.zeros(1, dtype=torch.int64, device="cuda")),
                 "_floor": torch.zeros(1, dtype=torch.int32, device="cuda"),
             }
@@ -235,6 +241,7 @@ class DatabaseSearch:
             if feed:
                 opts.d_arrived, opts.arrive_jobs, opts.arrive_epoch = (feed[0].data_ptr(),
                                                                        feed[1], feed[2])
+                opts.arrive_timeout_ns = self.feed_timeout_ns
         _lib.check(L.sw_db_align(C.byref(self.plan16), _ptr(self.prof16), self.kid, sch.gap_open,
                                  sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
                                  _ptr(d.length), _ptr(order), n, None, _ptr(o["score"]),
@@ -281,6 +288,25 @@ class DatabaseSearch:
                                  None, None, None, st))
         self.launches += 2
 
+    def _refeed(self, n: int, floor: bool) -> None:
+        """Re-run the jobs a streamed launch gave up on (FLAG_FEED_TIMEOUT: their
+        chunk had not arrived in time) with an ordinary 16-bit launch over the
+        device-collected list, after the copies are done. Without a timeout the
+        list is empty and the launch exits at once (no host sync either way)."""
+        L = _lib.load()
+        p, d, o, sch = self.prof, self.dev, self.out, self.scheme
+        st = _stream()
+        lst, cnt = o["_refeed"]
+        _lib.check(L.sw_collect_flagged(_ptr(o["flags"]), n, _lib.FLAG_FEED_TIMEOUT, _ptr(lst),
+                                        _ptr(cnt), st))
+        opts = _lib.DbOpts(d_coord_floor=o["_floor"].data_ptr()) if floor else None
+        _lib.check(L.sw_db_align(C.byref(self.plan16), _ptr(self.prof16), self.kid, sch.gap_open,
+                                 sch.gap_extend, p.bias, p.max_sub, _ptr(d.codes), _ptr(d.start),
+                                 _ptr(d.length), _ptr(lst), 0, _ptr(cnt), _ptr(o["score"]),
+                                 _ptr(o["ref_end"]), _ptr(o["query_end"]), _ptr(o["flags"]),
+                                 None, None, C.byref(opts) if opts else None, st))
+        self.launches += 2
+
     def align(self) -> dict:
         assert self.dev is not None and self.prof is not None, "upload() and set_query() first"
         n = self.dev.n
@@ -292,13 +318,20 @@ class DatabaseSearch:
         return self.out
 
     def search_streamed(self, packed: PackedDb, n_chunks: int = 64,
-                        floor_from: torch.Tensor | None = None) -> dict:
+                        floor_from: torch.Tensor | None = None,
+                        _starve_copy: bool = False) -> dict:
         """End-to-end form for a host-resident (pinned) database, one kernel launch:
         the copy stream uploads chunk c (residues, starts, lengths, ids) and then
         its arrival flag; the striped kernel, launched at once, makes each task
         wait for the chunk holding its targets, so the H2D transfer overlaps the
         alignment with no per-chunk launch tails. Requires set_query(); returns
-        the result dict."""
+        the result dict.
+
+        CUDA does not promise that the copies run while the kernel does (profilers,
+        CUDA_LAUNCH_BLOCKING and sanitizers serialise them): a task whose chunk is
+        late by ``feed_timeout_ns`` aborts the feed, the launch flags every job it
+        did not align with FLAG_FEED_TIMEOUT, and those jobs are re-run here once
+        the copies are done -- results are exact either way, never silently 0."""
         assert self.prof is not None, "set_query() first"
         self._ensure_buffers(packed)
         d, o = self.dev, self.out
@@ -315,13 +348,11 @@ class DatabaseSearch:
             self._arrived = torch.zeros(max(n_chunks, 64), dtype=torch.int32, device="cuda")
             self._epoch = 0
         self._epoch += 1
-        key = (id(packed), n, cj)
-        if getattr(self, "_chunk_key", None) != key:  # residue ranges of the chunks
-            st, ln = packed.start.numpy(), packed.length.numpy()
-            self._chunks = [(c * cj, min(n, (c + 1) * cj), int(st[c * cj]),
-                             int(st[min(n, (c + 1) * cj) - 1] + ln[min(n, (c + 1) * cj) - 1]))
-                            for c in range(n_chunks)]
-            self._chunk_key = key
+        # residue ranges of the chunks (recomputed every call: O(n_chunks))
+        st, ln = packed.start.numpy(), packed.length.numpy()
+        chunks = [(c * cj, min(n, (c + 1) * cj), int(st[c * cj]),
+                   int(st[min(n, (c + 1) * cj) - 1] + ln[min(n, (c + 1) * cj) - 1]))
+                  for c in range(n_chunks)]
         marks = torch.full((n_chunks,), self._epoch, dtype=torch.int32).pin_memory()
         copy.wait_stream(cur)  # buffers may still be read by a previous step
         # launch first (its tasks wait for their chunk), then feed the chunks
@@ -336,14 +367,17 @@ class DatabaseSearch:
             floor_on = bool(sample)
         self._launch16(n, floor=floor_on, sample=sample, order=order,
                        feed=(self._arrived, cj, self._epoch))
+        if _starve_copy:  # test hook: the copies may only start after the kernel
+            copy.wait_stream(cur)
         with torch.cuda.stream(copy):
-            for c, (a, b, ra, rb) in enumerate(self._chunks):
+            for c, (a, b, ra, rb) in enumerate(chunks):
                 d.codes[ra:rb].copy_(packed.codes[ra:rb], non_blocking=True)
                 d.start[a:b].copy_(packed.start[a:b], non_blocking=True)
                 d.length[a:b].copy_(packed.length[a:b], non_blocking=True)
                 self._arrived[c:c + 1].copy_(marks[c:c + 1], non_blocking=True)
             d.ids[:n].copy_(packed.ids, non_blocking=True)  # for top-k only
         cur.wait_stream(copy)  # ids before topk; the copy stream's work before the next step
+        self._refeed(n, floor_on)  # jobs whose chunk timed out, now that it is resident
         self._rescue(n)
         return o
 

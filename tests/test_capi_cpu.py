@@ -136,3 +136,40 @@ def test_product_path_has_no_cpu_fallback(monkeypatch):
     sch = ScoringScheme.match_mismatch(Alphabet("ACGT"), 2, -1, 3, 1)
     with pytest.raises(_lib.NativeUnavailable):
         align.align_pair("scan", 8, [0, 1, 2], [0, 1], sch)
+
+
+def _header_arity() -> dict[str, int]:
+    with open(os.path.join(REPO, "include", "swscan_b200.h")) as fh:
+        text = re.sub(r"/\*.*?\*/", "", fh.read(), flags=re.S)
+    out = {}
+    for m in re.finditer(r"(?:int32_t|int64_t|const char\*)\s+(sw_\w+)\(([^)]*)\);", text):
+        args = m.group(2).strip()
+        out[m.group(1)] = 0 if args in ("", "void") else args.count(",") + 1
+    return out
+
+
+def integration_stub() -> str:
+    """The ctypes stub of INTEGRATION.md §2, verbatim."""
+    with open(os.path.join(REPO, "INTEGRATION.md")) as fh:
+        text = fh.read()
+    block = text.split("<!-- stub:begin -->", 1)[1].split("<!-- stub:end -->", 1)[0]
+    return block.split("```python", 1)[1].rsplit("```", 1)[0]
+
+
+def test_integration_stub_signatures(monkeypatch):
+    """The documented drop-in stub binds every entry point with the header's arity
+    (the old stub passed 23 arguments to the 21-parameter sw_db_align)."""
+    from paper_1909_00899_b200 import _lib
+
+    _lib.build()
+    monkeypatch.setenv("SWSCAN_B200_LIB", _lib.LIB_PATH)
+    ns: dict = {}
+    exec(compile(integration_stub(), "INTEGRATION.md", "exec"), ns)
+    arity = _header_arity()
+    assert arity["sw_db_align"] == 21
+    for name in ("sw_plan_query", "sw_profile_build", "sw_db_align"):
+        assert len(getattr(ns["_L"], name).argtypes) == arity[name], name
+    # and the package's own binding agrees with the header everywhere
+    L = _lib.load()
+    for name in _lib.EXPORTS:
+        assert len(getattr(L._lib, name).argtypes) == arity[name], name
