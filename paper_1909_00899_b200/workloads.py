@@ -191,15 +191,27 @@ def config2(n_targets: int = 1_000_000, seed: int = SEEDS[2]) -> DbWorkload:
                        "composition": "synthetic-stand-in (Robinson-Robinson not in container)"})
 
 
-def config3(n_pairs: int = 1 << 24, seed: int = SEEDS[3], chunk: int = 1 << 20) -> BatchWorkload:
-    """Short reads: 150 nt read vs 300 nt window, 1% subs, 0.1% indels (1..3)."""
-    rng = np.random.default_rng(seed)
+C3_CHUNK = 1 << 16  # config 3 pairs per independently seeded generator block
+
+
+def config3(n_pairs: int = 1 << 24, seed: int = SEEDS[3], start: int = 0,
+            stop: int | None = None) -> BatchWorkload:
+    """Short reads: 150 nt read vs 300 nt window, 1% subs, 0.1% indels (1..3).
+
+    Pairs are generated in blocks of C3_CHUNK, block b from its own generator
+    ``default_rng((seed, b))``, so any pair range [start, stop) -- a rank's shard
+    -- is generated without the pairs before it, and a smaller n_pairs is a prefix
+    of the full batch. Returns the pairs [start, stop) (default: all n_pairs)."""
+    stop = n_pairs if stop is None else min(stop, n_pairs)
+    start = max(0, min(start, stop))
     W, R = 300, 150
-    flat_r = np.empty(n_pairs * W, dtype=np.uint8)
-    flat_q = np.empty(n_pairs * R, dtype=np.uint8)
-    for s in range(0, n_pairs, chunk):
-        e = min(n_pairs, s + chunk)
-        n = e - s
+    n_out = stop - start
+    flat_r = np.empty(n_out * W, dtype=np.uint8)
+    flat_q = np.empty(n_out * R, dtype=np.uint8)
+    for blk in range(start // C3_CHUNK, -(-stop // C3_CHUNK)):
+        rng = np.random.default_rng((seed, blk))
+        b0 = blk * C3_CHUNK
+        n = min(C3_CHUNK, n_pairs - b0)
         win = rng.integers(0, 4, (n, W), dtype=np.uint8)
         off = rng.integers(0, W - R - 16 + 1, n)
         # indel events: per read position, Bernoulli(0.001); type and length
@@ -223,13 +235,15 @@ def config3(n_pairs: int = 1 << 24, seed: int = SEEDS[3], chunk: int = 1 << 20) 
         read[use_rnd] = rnd[use_rnd]
         subs = rng.random((n, R)) < 0.01
         read[subs] = (read[subs] + rng.integers(1, 4, int(subs.sum()))) % 4
-        flat_r[s * W:e * W] = win.reshape(-1)
-        flat_q[s * R:e * R] = read.reshape(-1)
-    q_off = np.arange(n_pairs + 1, dtype=np.int64) * R
-    r_off = np.arange(n_pairs + 1, dtype=np.int64) * W
+        a, b = max(start, b0), min(stop, b0 + n)  # the part of this block in [start, stop)
+        flat_r[(a - start) * W:(b - start) * W] = win[a - b0:b - b0].reshape(-1)
+        flat_q[(a - start) * R:(b - start) * R] = read[a - b0:b - b0].reshape(-1)
+    q_off = np.arange(n_out + 1, dtype=np.int64) * R
+    r_off = np.arange(n_out + 1, dtype=np.int64) * W
     scheme = ScoringScheme.match_mismatch(DNA4, 2, -4, 6, 1)
     return BatchWorkload("config3-short-reads", flat_q, q_off, flat_r, r_off, scheme, DNA4, seed,
-                         {"read_len": R, "window": W})
+                         {"read_len": R, "window": W, "pairs": [start, stop],
+                          "n_pairs_total": n_pairs})
 
 
 def config4(n_ref: int = 100_000, m: int = 2048, seed: int = SEEDS[4]) -> PairWorkload:

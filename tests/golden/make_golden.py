@@ -129,14 +129,42 @@ def runner_fixtures() -> None:
         json.dump(out, fh, indent=1)
 
 
+def config3_fixtures(C, cfg: dict) -> None:
+    """Config-3-shaped cases (2,000 pairs of the seeded generator) from the
+    reference's batch drivers (src/_compiled.py:491-529)."""
+    from paper_1909_00899_b200 import workloads as W
+
+    w3 = W.config3(n_pairs=2000)
+    cfg["c3_inputs_sha256"] = np.array(sha(w3.flat_q, w3.q_off, w3.flat_r, w3.r_off))
+    n3 = w3.n_pairs
+    m3 = np.full(n3, 2, np.int64)
+    x3 = np.full(n3, -4, np.int64)
+    g3 = np.full(n3, 6, np.int64)
+    e3 = np.full(n3, 1, np.int64)
+    fq3, fr3 = w3.flat_q.astype(np.int16), w3.flat_r.astype(np.int16)
+    cfg["c3_scalar"] = C.batch_oracle_scores(fq3, w3.q_off, fr3, w3.r_off, m3, x3, g3, e3)
+    for kid, kern in ((0, "lazyf"), (2, "scan")):
+        for p in (8, 16):
+            sc, ov, _ = C.batch_align(kid, p, fq3, w3.q_off, fr3, w3.r_off, m3, x3, g3, e3)
+            cfg[f"c3_{kern}_p{p}"] = sc.astype(np.int64)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--full-config5", action="store_true",
                     help="also score the full 65,536 x 1,048,576 config 5 (minutes)")
     ap.add_argument("--only-runner", action="store_true",
                     help="only regenerate the runner TSV fixtures")
+    ap.add_argument("--only-config3", action="store_true",
+                    help="only refresh the config-3 keys of configs.npz")
     args = ap.parse_args()
     swscan, C = _import_reference()
+    if args.only_config3:
+        cfg = dict(np.load(os.path.join(HERE, "configs.npz")))
+        config3_fixtures(C, cfg)
+        np.savez_compressed(os.path.join(HERE, "configs.npz"), **cfg)
+        print("config 3 fixtures refreshed")
+        return
     runner_fixtures()
     if args.only_runner:
         return
@@ -323,20 +351,7 @@ def main() -> None:
     cfg["c2_scan_p16"] = np.array(scan2, np.int64)
     cfg["c2_lazyf_p16"] = np.array(lz2, np.int64)
 
-    w3 = W.config3(n_pairs=2000)
-    cfg["c3_inputs_sha256"] = np.array(sha(w3.flat_q, w3.q_off, w3.flat_r, w3.r_off))
-    n3 = w3.n_pairs
-    m3 = np.full(n3, 2, np.int64)
-    x3 = np.full(n3, -4, np.int64)
-    g3 = np.full(n3, 6, np.int64)
-    e3 = np.full(n3, 1, np.int64)
-    fq3, fr3 = w3.flat_q.astype(np.int16), w3.flat_r.astype(np.int16)
-    cfg["c3_scalar"] = C.batch_oracle_scores(fq3, w3.q_off, fr3, w3.r_off, m3, x3, g3, e3)
-    for kid, kern in ((0, "lazyf"), (2, "scan")):
-        for p in (8, 16):
-            sc, ov, _ = C.batch_align(kid, p, fq3, w3.q_off, fr3, w3.r_off, m3, x3, g3, e3)
-            cfg[f"c3_{kern}_p{p}"] = sc.astype(np.int64)
-
+    config3_fixtures(C, cfg)
     w4 = W.config4()
     s4 = scheme_of(w4)
     q16, r16 = w4.query.astype(np.int16), w4.ref.astype(np.int16)

@@ -53,3 +53,27 @@ def mm_matrix(match: int, mismatch: int, k: int = 4) -> np.ndarray:
     m = np.full((k, k), mismatch, dtype=np.int8)
     np.fill_diagonal(m, match)
     return m
+
+
+def result_digest(score, ref_end, query_end, blocks: int = 256) -> dict:
+    """Digest of full-size results (tests/golden/make_fullsize.py): sha256 over the
+    int32 (score, ref_end, query_end) arrays plus per-block digests (16 hex chars
+    each, contiguous blocks of items) so a mismatch is localised."""
+    s = np.ascontiguousarray(score, dtype=np.int32)
+    r = np.ascontiguousarray(ref_end, dtype=np.int32)
+    q = np.ascontiguousarray(query_end, dtype=np.int32)
+    n = s.shape[0]
+    bounds = [n * b // blocks for b in range(blocks + 1)]
+    bd = [sha(s[a:b], r[a:b], q[a:b])[:16] for a, b in zip(bounds[:-1], bounds[1:])]
+    return {"n": int(n), "digest": sha(s, r, q), "blocks": blocks, "block_digests": bd,
+            "score_sum": int(s.astype(np.int64).sum()), "score_max": int(s.max()) if n else 0}
+
+
+def digest_mismatch(got: dict, want: dict) -> str:
+    """Human-readable difference between two result_digest dicts ('' when equal)."""
+    if got["digest"] == want["digest"]:
+        return ""
+    bad = [i for i, (a, b) in enumerate(zip(got["block_digests"], want["block_digests"])) if a != b]
+    return (f"digest differs in {len(bad)} of {want['blocks']} blocks (first {bad[:8]}); "
+            f"score sum {got['score_sum']} vs {want['score_sum']}, max {got['score_max']} vs "
+            f"{want['score_max']}")
