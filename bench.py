@@ -1,17 +1,30 @@
-"""Benchmark: config 2 protein database search (BASELINE.json configs[1]) in GCUPS.
+"""Benchmark: GCUPS of the five BASELINE.json configurations (default: config 2).
 
-One step = one query (464 residues) against the whole synthetic 1,000,000-
-target database (sharded over ranks when --gpus > 1): profile build, 16-bit
-striped scan kernel, device-side 32-bit rescue, per-rank top-100, NCCL
-all_gather top-100 merge. Cells = 464 x total target residues (padding
-excluded). Inputs (359 MB of residues) exceed the 126 MB L2, so no flush is
-needed between steps.
+  python bench.py [--config 1..5] [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+One step = one pass of the hot path over one batch of the configuration's
+synthetic input (seeded generators, paper_1909_00899_b200/workloads.py):
 
---impl reference times the reference algorithm's CPU implementation (the C
-restatement in oracle/, scan kernel p=16, OpenMP over every host core) on a
-bounded sample of the same workload.
+* config 2 (the headline, BASELINE.json configs[1]): one 464-residue query
+  against the 1,000,000-target database -- profile build, 16-bit striped scan
+  kernel (in-kernel coordinate floor), device-side 32-bit rescue, per-rank
+  top-100, NCCL all_gather top-100 merge. Database sharded over ranks.
+* config 3: all 16,777,216 read/window pairs, score-only (the metric), 16-bit
+  pairs kernel + 32-bit rescue. Pairs sharded over ranks (each rank generates
+  only its own pairs), no data-path collective.
+* configs 1, 4, 5: one pair (replicas only at N > 1): the scan kernel, with the
+  lazy-F kernel and the other exact paths timed beside it ("variants").
+
+Cells = sum of m x n over pairs, padding excluded. `value` = device time with
+inputs resident in HBM (CUDA events on the launching stream, barrier +
+synchronize around the timed region, max over ranks); `e2e` = the same metric
+through the public API from host buffers, copies inside the timed region.
+Inputs larger than the 126 MB L2 (configs 2, 3) run back to back; the small
+single-pair inputs get an L2 flush (a 256 MB write) between steps, outside the
+events. `--impl reference` times the reference's own CPU implementation (the
+numba kernels of swscan from baseline/_ref under a process pool over the host
+cores; the C restatement in oracle/ when that is absent) on a bounded sample of
+the same workload.
 """
 
 from __future__ import annotations
@@ -34,18 +47,31 @@ if REPO not in sys.path:
 METRIC = "GCUPS (score-only SW, device-timed, whole box)"
 UNIT = "GCUPS"
 TOPK = 100
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
+
+CONFIGS = {
+    1: {"workload": "config1-single-pair-dna", "dtype": "s16x2", "width": 16},
+    2: {"workload": "config2-protein-db", "dtype": "s16x2", "width": 16},
+    3: {"workload": "config3-short-reads", "dtype": "s16x2", "width": 16},
+    4: {"workload": "config4-adversarial-f", "dtype": "s32", "width": 32},
+    5: {"workload": "config5-long-pair", "dtype": "s32", "width": 32},
+}
 
 
 def parse():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n-targets", type=int, default=1_000_000)
+    ap.add_argument("--n-targets", type=int, default=1_000_000, help="config 2 database size")
+    ap.add_argument("--n-pairs", type=int, default=1 << 24, help="config 3 batch size")
     ap.add_argument("--kernel", default="scan", choices=["scan", "lazyf"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-port", action="store_true",
+                    help="reference arm: time the C restatement instead of the numba reference")
     return ap.parse_args()
 
 
@@ -65,7 +91,7 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index = index
-        self.rows: list[tuple[float, float, int]] = []
+        self.rows: list[tuple[float, float, int, float]] = []
         self._stop = threading.Event()
         self.thread = None
         self.handle = None
@@ -141,87 +167,634 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"unavailable: {e}"]}
 
 
-def cpu_baseline(w, seconds: float) -> dict:
-    """The reference algorithm on the host cores: C restatement of _align_scan_c
-    (oracle/, OpenMP over all cores) on a bounded prefix of the same database."""
+# ---------------------------------------------------------------------------------------
+# workloads (shared by both arms: same seeds, same shapes)
+
+
+def load_workload(cfg: int, args, rank: int = 0, world: int = 1):
+    from paper_1909_00899_b200 import workloads as W
+
+    if cfg == 1:
+        return W.config1()
+    if cfg == 2:
+        return W.config2(n_targets=args.n_targets)
+    if cfg == 3:
+        from paper_1909_00899_b200.search import shard_pairs
+
+        a, b = shard_pairs(args.n_pairs, rank, world)
+        return W.config3(n_pairs=args.n_pairs, start=a, stop=b)
+    if cfg == 4:
+        return W.config4()
+    return W.config5()
+
+
+def total_cells(cfg: int, w, args) -> int:
+    if cfg == 3:
+        return 150 * 300 * args.n_pairs
+    return int(w.cells)
+
+
+def arm_config(cfg: int, w, args, world: int) -> dict:
+    """The workload description both arms report (the reference arm times a bounded
+    sample of the same workload; the sample is described in its cpu_baseline)."""
+    base = {"workload": CONFIGS[cfg]["workload"], "cells": total_cells(cfg, w, args),
+            "scheme": {"gap_open": w.scheme.gap_open, "gap_extend": w.scheme.gap_extend,
+                       "matrix": (w.notes.get("matrix") or
+                                  f"match {w.scheme.matrix[0][0]} / mismatch {w.scheme.matrix[0][1]}")},
+            "seed": hex(w.seed)}
+    if cfg == 2:
+        base.update({"query_len": int(w.query.shape[0]), "n_targets": args.n_targets,
+                     "residues": int(w.offsets[-1]), "kernel": args.kernel, "top_k": TOPK,
+                     "l2": "inputs 359 MB > 126 MB L2 (no flush)",
+                     "parallelism": f"db-shard x{world}"})
+    elif cfg == 3:
+        base.update({"pairs": args.n_pairs, "read_len": 150, "window": 300,
+                     "output": "score-only (metric); coordinates timed as a variant",
+                     "l2": "inputs 7.55 GB > 126 MB L2 (no flush)",
+                     "parallelism": f"pair-shard x{world}"})
+    else:
+        base.update({"query_len": int(w.query.shape[0]), "ref_len": int(w.ref.shape[0]),
+                     "l2": "L2 flushed between steps (256 MB write, outside the events)",
+                     "parallelism": f"replicas x{world}"})
+    return base
+
+
+# ---------------------------------------------------------------------------------------
+# CPU baseline (the C restatement of the reference kernels, all host cores)
+
+
+def cpu_baseline(cfg: int, w, seconds: float) -> dict:
+    """The reference algorithm on the host cores: the C restatement of
+    _align_scan_c / batch_align (oracle/, OpenMP over all cores) on a bounded
+    sample of the same workload (single pairs: one core, the pair cannot split)."""
     from oracle import oracle as O
 
     threads = O.n_threads()
-    prof, bias = O.build_profile(w.query, w.scheme.as_array(), 16)
+    sub = w.scheme.as_array()
     go, ge = w.scheme.gap_open, w.scheme.gap_extend
-    n_take, done_cells, elapsed, t_start = 256, 0, 0.0, 0
-    while elapsed < seconds and t_start < w.n_targets:
-        t_end = min(w.n_targets, t_start + n_take)
-        sub_off = w.offsets[t_start:t_end + 1] - w.offsets[t_start]
-        sub_db = w.db[w.offsets[t_start]:w.offsets[t_end]]
-        t0 = time.perf_counter()
-        O.db_striped("scan", prof, bias, sub_db, sub_off, go, ge, threads=threads)
-        elapsed += time.perf_counter() - t0
-        done_cells += int(sub_off[-1]) * w.query.shape[0]
-        t_start = t_end
-        n_take *= 2
-    return {"value": done_cells / elapsed / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first {t_start} of {w.n_targets} targets ({done_cells / 1e9:.2f} Gcells, "
-                      f"{elapsed:.1f} s), scan kernel p=16 (C restatement of _align_scan_c, "
-                      f"OpenMP {threads} threads)"}
+    done, elapsed = 0, 0.0
+    if cfg == 2:
+        prof, bias = O.build_profile(w.query, sub, 16)
+        n_take, t_start = 256, 0
+        while elapsed < seconds and t_start < w.n_targets:
+            t_end = min(w.n_targets, t_start + n_take)
+            sub_off = w.offsets[t_start:t_end + 1] - w.offsets[t_start]
+            sub_db = w.db[w.offsets[t_start]:w.offsets[t_end]]
+            t0 = time.perf_counter()
+            O.db_striped("scan", prof, bias, sub_db, sub_off, go, ge, threads=threads)
+            elapsed += time.perf_counter() - t0
+            done += int(sub_off[-1]) * w.query.shape[0]
+            t_start = t_end
+            n_take *= 2
+        sample = (f"first {t_start} of {w.n_targets} targets, scan kernel p=16 (C restatement of "
+                  f"_align_scan_c), OpenMP {threads} threads")
+        cores = threads
+    elif cfg == 3:
+        n_take, a = 4096, 0
+        while elapsed < seconds and a < w.n_pairs:
+            b = min(w.n_pairs, a + n_take)
+            qo = w.q_off[a:b + 1] - w.q_off[a]
+            ro = w.r_off[a:b + 1] - w.r_off[a]
+            t0 = time.perf_counter()
+            O.batch_striped("scan", 8, w.flat_q[w.q_off[a]:w.q_off[b]], qo,
+                            w.flat_r[w.r_off[a]:w.r_off[b]], ro, sub=sub, go=go, ge=ge,
+                            threads=threads)
+            elapsed += time.perf_counter() - t0
+            done += int(np.dot(np.diff(qo), np.diff(ro)))
+            a = b
+            n_take *= 2
+        sample = (f"first {a} of {w.n_pairs} pairs, batch_align scan p=8 (C restatement), "
+                  f"OpenMP {threads} threads")
+        cores = threads
+    else:
+        p = 16 if cfg == 1 else 64
+        prof, bias = O.build_profile(w.query, sub, p)
+        n_cols = w.ref.shape[0]
+        cols = n_cols if cfg != 5 else 16384
+        reps = 0
+        while elapsed < seconds and (reps == 0 or cols == n_cols):
+            t0 = time.perf_counter()
+            O.align_prebuilt("scan", prof, bias, w.ref[:cols], go, ge)
+            elapsed += time.perf_counter() - t0
+            done += cols * int(w.query.shape[0])
+            reps += 1
+            if cols < n_cols and elapsed < seconds / 2:
+                cols = min(n_cols, cols * 2)
+        sample = (f"{reps} run(s) of the scan kernel p={p} (C restatement of _align_scan_c, one "
+                  f"core) over the query x the first {cols} reference residues")
+        cores = 1
+    return {"value": round(done / elapsed / 1e9, 4), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{sample} ({done / 1e9:.2f} Gcells, {elapsed:.1f} s)"}
 
 
-def arm_config(w, args, world: int) -> dict:
-    """The workload description both arms report (the reference arm times a bounded
-    sample of the same workload; the sample is described in its cpu_baseline)."""
-    return {"workload": "config2-protein-db", "query_len": int(w.query.shape[0]),
-            "n_targets": args.n_targets, "residues": int(w.offsets[-1]),
-            "cells": int(w.query.shape[0]) * int(w.offsets[-1]), "kernel": args.kernel,
-            "top_k": TOPK, "matrix": "synthetic-stand-in (BLOSUM62 not in container)",
-            "gaps": "open 11, extend 1 (reference convention)",
-            "l2": "inputs 359 MB > 126 MB L2 (no flush)", "parallelism": f"db-shard x{world}"}
+# ---------------------------------------------------------------------------------------
+# reference arm: the reference's own numba kernels (swscan._compiled), process pool
+
+
+def _ref_module():
+    """swscan from baseline/_ref (pip-installed from /root/reference, git-ignored);
+    None when absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "swscan")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/swscan_numba_cache")
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        from swscan import _compiled
+        from swscan.scoring import ScoringScheme
+    except Exception:  # noqa: BLE001
+        return None
+    return _compiled, ScoringScheme
+
+
+_POOL_STATE: dict = {}
+
+
+def _ref_db_chunk(bounds):
+    """Worker: the reference runner's per-pair call (align_prebuilt, src/runner.py:146-151)
+    over a range of database targets."""
+    C, scheme, prof, bias, db, offs = (_POOL_STATE[k] for k in
+                                       ("C", "scheme", "prof", "bias", "db", "offs"))
+    a, b = bounds
+    s = 0
+    for t in range(a, b):
+        s += C.align_prebuilt("scan", prof, bias, db[offs[t]:offs[t + 1]], scheme).score
+    return s
+
+
+def _ref_pairs_chunk(bounds):
+    """Worker: the reference's batch driver (batch_align, src/_compiled.py:504-529)."""
+    C, fq, qo, fr, ro = (_POOL_STATE[k] for k in ("C", "fq", "qo", "fr", "ro"))
+    a, b = bounds
+    n = b - a
+    ones = np.ones(n, np.int64)
+    s, _, _ = C.batch_align(2, 8, fq, qo[a:b + 1], fr, ro[a:b + 1], 2 * ones, -4 * ones,
+                            6 * ones, ones)
+    return int(s.sum())
 
 
 def run_reference(args) -> None:
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    from oracle import oracle as O
-    from paper_1909_00899_b200 import workloads as W
-
-    w = W.config2(n_targets=args.n_targets)
-    threads = O.n_threads()
-    prof, bias = O.build_profile(w.query, w.scheme.as_array(), 16)
-    go, ge = w.scheme.gap_open, w.scheme.gap_extend
-    # bounded sample per step: enough targets for ~2 s of all-core CPU work
-    t_end, cells = 4096, 0
-    probe_off = w.offsets[:t_end + 1]
-    t0 = time.perf_counter()
-    O.db_striped("scan", prof, bias, w.db[: probe_off[-1]], probe_off, go, ge, threads=threads)
-    rate = int(probe_off[-1]) * w.query.shape[0] / max(1e-6, time.perf_counter() - t0)
-    want = 2.0 * rate / w.query.shape[0]
-    t_end = int(np.searchsorted(w.offsets, want))
-    t_end = max(256, min(w.n_targets, t_end))
-    off = w.offsets[: t_end + 1]
-    db = w.db[: off[-1]]
-    cells = int(off[-1]) * w.query.shape[0]
+    cfg = args.config
+    w = load_workload(cfg, args)
+    ref = None if args.ref_port else _ref_module()
+    cores = len(os.sched_getaffinity(0))
+    if ref is None:
+        kind, impl = "port", "C restatement of the reference kernels (oracle/), OpenMP"
+        timer = _port_timer(cfg, w)
+        cores_used = timer.cores
+    else:
+        kind, impl = "reference", "reference numba kernels (swscan._compiled from baseline/_ref)"
+        timer = _numba_timer(cfg, w, ref, cores)
+        cores_used = timer.cores
+    timer.calibrate(2.0)
     for _ in range(args.warmup):
-        O.db_striped("scan", prof, bias, db, off, go, ge, threads=threads)
+        timer.step()
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        O.db_striped("scan", prof, bias, db, off, go, ge, threads=threads)
+        timer.step()
         times.append(time.perf_counter() - t0)
+    timer.close()
     total = sum(times)
-    value = cells * args.steps / total / 1e9
-    sample = (f"first {t_end} of {w.n_targets} targets per step ({cells / 1e9:.2f} Gcells), "
-              f"scan kernel p=16, C restatement of _align_scan_c, OpenMP {threads} threads")
+    value = timer.cells * args.steps / total / 1e9
+    sample = f"{timer.sample} per step ({timer.cells / 1e9:.3f} Gcells); {impl}, {cores_used} cores"
     print(json.dumps({
-        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16",
         "data": "synthetic", "impl": "reference",
-        "config": arm_config(w, args, world),
-        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "port",
+        "config": arm_config(cfg, w, args, world),
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores_used, "kind": kind,
                          "sample": sample},
-        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+class _port_timer:
+    def __init__(self, cfg, w):
+        from oracle import oracle as O
+
+        self.O, self.cfg, self.w = O, cfg, w
+        self.cores = O.n_threads() if cfg in (2, 3) else 1
+        sub = w.scheme.as_array()
+        self.sub, self.go, self.ge = sub, w.scheme.gap_open, w.scheme.gap_extend
+        if cfg == 2:
+            self.prof, self.bias = O.build_profile(w.query, sub, 16)
+        elif cfg != 3:
+            self.prof, self.bias = O.build_profile(w.query, sub, 16 if cfg == 1 else 64)
+
+    def _run(self, k):
+        O, w = self.O, self.w
+        if self.cfg == 2:
+            off = w.offsets[:k + 1]
+            O.db_striped("scan", self.prof, self.bias, w.db[:off[-1]], off, self.go, self.ge,
+                         threads=self.cores)
+            return int(off[-1]) * w.query.shape[0], f"first {k} of {w.n_targets} targets"
+        if self.cfg == 3:
+            O.batch_striped("scan", 8, w.flat_q[:w.q_off[k]], w.q_off[:k + 1],
+                            w.flat_r[:w.r_off[k]], w.r_off[:k + 1], sub=self.sub, go=self.go,
+                            ge=self.ge, threads=self.cores)
+            return k * 45000, f"first {k} of {w.n_pairs} pairs"
+        O.align_prebuilt("scan", self.prof, self.bias, w.ref[:k], self.go, self.ge)
+        return k * w.query.shape[0], f"query x first {k} of {w.ref.shape[0]} reference residues"
+
+    def calibrate(self, seconds):
+        """Grow the sample until one run takes > 0.2 s, then size it for `seconds`."""
+        w = self.w
+        full = (w.n_targets if self.cfg == 2 else w.n_pairs if self.cfg == 3
+                else int(w.ref.shape[0]))
+        k = max(1, min(full, 256 if self.cfg in (2, 3) else 1024))
+        while True:
+            t0 = time.perf_counter()
+            cells, _ = self._run(k)
+            dt = time.perf_counter() - t0
+            if dt > 0.2 or k >= full:
+                break
+            k = min(full, k * 4)
+        self.k = max(1, min(full, int(k * seconds / max(dt, 1e-3))))
+        self.cells, self.sample = self._run(self.k)
+
+    def step(self):
+        self._run(self.k)
+
+    def close(self):
+        pass
+
+
+class _numba_timer:
+    """The reference's own numba kernels: database targets / pair chunks spread over
+    a fork-based process pool (numba holds the GIL; the parent compiles first so the
+    workers inherit the compiled dispatchers); a single pair runs on one core."""
+
+    def __init__(self, cfg, w, ref, cores):
+        C, Scheme = ref
+        self.C, self.cfg, self.w = C, cfg, w
+        self.scheme = Scheme(w.scheme.matrix, w.scheme.gap_open, w.scheme.gap_extend)
+        self.cores = cores if cfg in (2, 3) else 1
+        self.pool = None
+        if cfg == 2:
+            q = w.query.astype(np.int16)
+            self.prof, self.bias = C.build_profile_arrays(q, self.scheme, 16)
+            _POOL_STATE.update(C=C, scheme=self.scheme, prof=self.prof, bias=self.bias,
+                               db=w.db.astype(np.int16), offs=w.offsets)
+            _ref_db_chunk((0, 2))
+        elif cfg == 3:
+            _POOL_STATE.update(C=C, fq=w.flat_q.astype(np.int16), qo=w.q_off,
+                               fr=w.flat_r.astype(np.int16), ro=w.r_off)
+            _ref_pairs_chunk((0, 2))
+        else:
+            p = 16 if cfg == 1 else 64
+            self.prof, self.bias = C.build_profile_arrays(w.query.astype(np.int16), self.scheme, p)
+            self.p = p
+            self.ref16 = w.ref.astype(np.int16)
+            C.align_prebuilt("scan", self.prof, self.bias, self.ref16[:64], self.scheme)
+        if self.cores > 1:
+            import multiprocessing as mp
+
+            self.pool = mp.get_context("fork").Pool(self.cores)
+
+    def _run(self, k):
+        w = self.w
+        if self.cfg in (2, 3):
+            parts = max(1, self.cores * 4)
+            bounds = [(k * i // parts, k * (i + 1) // parts) for i in range(parts)]
+            fn = _ref_db_chunk if self.cfg == 2 else _ref_pairs_chunk
+            if self.pool is not None:
+                self.pool.map(fn, bounds)
+            else:
+                [fn(b) for b in bounds]
+            if self.cfg == 2:
+                return (int(w.offsets[k]) * w.query.shape[0],
+                        f"first {k} of {w.n_targets} targets (align_prebuilt('scan', p=16) per target)")
+            return k * 45000, f"first {k} of {w.n_pairs} pairs (batch_align scan p=8)"
+        self.C.align_prebuilt("scan", self.prof, self.bias, self.ref16[:k], self.scheme)
+        return (k * w.query.shape[0],
+                f"align_prebuilt('scan', p={self.p}): query x first {k} of {w.ref.shape[0]} "
+                f"reference residues")
+
+    calibrate = _port_timer.calibrate
+    step = _port_timer.step
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.close()
+            self.pool.join()
+
+
+# ---------------------------------------------------------------------------------------
+# device arm
+
+
+class Timer:
+    """Device time of `fn` over K steps: per-step CUDA events on the launching
+    stream, optional L2 flush outside the events, max over ranks."""
+
+    def __init__(self, stream, world, backend, flush: bool):
+        import torch
+
+        self.torch, self.stream, self.world, self.backend = torch, stream, world, backend
+        self.flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if flush else None
+
+    def run(self, fn, steps: int) -> float:
+        torch = self.torch
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        out = None
+        for e0, e1 in evs:
+            if self.flush_buf is not None:
+                self.flush_buf.fill_(1)
+            e0.record(self.stream)
+            out = fn()
+            e1.record(self.stream)
+        torch.cuda.synchronize()
+        ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+        self.last = out
+        return self.max_over_ranks(ms)
+
+    def max_over_ranks(self, ms: float) -> float:
+        if self.world > 1:
+            import torch.distributed as dist
+
+            t = self.torch.tensor([ms], device="cuda" if self.backend == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+
+def dpx_peaks(L, stream) -> dict:
+    """Live DPX issue peak (cell-update instruction mix on every SM): 6
+    lane-instructions per cell, 2 cells per instruction in 16x2, 1 in 32-bit."""
+    import torch
+
+    from paper_1909_00899_b200.align import _ptr, _stream
+
+    scratch = torch.zeros(256, dtype=torch.int32, device="cuda")
+    L.sw_dpx_probe(1, 1000, _ptr(scratch), _stream())
+    torch.cuda.synchronize()
+    res = {}
+    for kind in (1, 0):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        n = L.sw_dpx_probe(kind, 20000, _ptr(scratch), _stream())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        res[kind] = n / (e0.elapsed_time(e1) * 1e-3)
+    return {"mix_instr_per_s": res[1], "viaddmnmx_s16x2_instr_per_s": res[0],
+            "peak16_gcups": res[1] * 2 / 6 / 1e9, "peak32_gcups": res[1] / 6 / 1e9}
+
+
+def hbm_peak() -> float:
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh).get("hbm_gbs", 6650.0))
+    except (OSError, ValueError):
+        return 6650.0
+
+
+# ---- config 2 -------------------------------------------------------------------------
+
+
+def device_config2(args, w, rank, world, timer, L):
+    import ctypes as C
+
+    import torch
+
+    from paper_1909_00899_b200 import _lib, search
+    from paper_1909_00899_b200.align import _ptr, _stream
+
+    m = int(w.query.shape[0])
+    ids = search.shard(w.offsets, rank, world)
+    packed = search.pack(w.db, w.offsets, ids)
+    rank_cells = m * packed.residues
+    eng = search.DatabaseSearch(w.scheme, kernel=args.kernel, coords="topk", k=TOPK)
+    eng.upload(packed)
+    eng.set_query(w.query)
+    torch.cuda.synchronize()
+
+    def step():
+        eng.rebuild_profile()
+        eng.align()
+        return search.merge_topk(eng.topk(TOPK), TOPK)
+
+    def kernel_only():
+        p, d, o = eng.prof, eng.dev, eng.out
+        _lib.check(L.sw_db_align(C.byref(eng.plan16), _ptr(eng.prof16), eng.kid, w.scheme.gap_open,
+                                 w.scheme.gap_extend, p.bias, p.max_sub, _ptr(d.codes),
+                                 _ptr(d.start), _ptr(d.length), None, d.n, None,
+                                 _ptr(o["score"]), _ptr(o["ref_end"]), _ptr(o["query_end"]),
+                                 _ptr(o["flags"]), None, None,
+                                 C.byref(_lib.DbOpts(d_coord_floor=o["_floor"].data_ptr())),
+                                 _stream()))
+
+    # under a profiler (ncu injects itself through CUDA_INJECTION64_PATH) kernels are
+    # serialised: a streamed launch would wait for its feed timeout before the re-run
+    profiled = "CUDA_INJECTION64_PATH" in os.environ
+
+    def e2e_step():
+        eng.set_query(w.query)
+        if profiled:
+            eng.upload(packed)
+            eng.align()
+        else:
+            eng.search_streamed(packed, n_chunks=64)  # one launch; tasks wait for their chunk
+        return search.merge_topk(eng.topk(TOPK), TOPK).cpu()
+
+    # what search_streamed copies per step: residues, starts, lengths, ids + the query
+    h2d = sum(int(t.numel() * t.element_size())
+              for t in (packed.codes, packed.start, packed.length, packed.ids)) + m
+    alg_bytes = packed.residues + packed.n * (8 + 4 + 4 + 4 + 4 + 4 + 1)
+    return {
+        "step": step, "kernel_only": kernel_only, "e2e_step": e2e_step, "engine": eng,
+        "rank_cells": rank_cells, "h2d": h2d, "d2h": TOPK * 4 * 8,
+        "kernel_name": (f"sw_striped_kernel<W16,T={eng.plan16.threads},L={eng.plan16.seg_len},"
+                        f"{args.kernel.upper()},ge={w.scheme.gap_extend}>"),
+        "width": 16, "alg_bytes": alg_bytes,
+        # dram__bytes_read+write per launch of this kernel (one ncu --set full capture at
+        # this config, profiles/r01i_config2_db_kernel.md)
+        "traffic": 509.05e6,
+        "extra_config": {"lanes": eng.plan16.lanes, "seg_len": eng.plan16.seg_len,
+                         "end_coords": "exact for every target scoring >= the in-kernel floor "
+                                       "(k-th best of a strided 1/16 sample: a superset of the "
+                                       "top-k); others score-only"},
+        "result": lambda out: {"top_hit": [int(x) for x in out[0].tolist()]},
+    }
+
+
+# ---- config 3 -------------------------------------------------------------------------
+
+
+def device_config3(args, w, rank, world, timer, L):
+    import torch
+
+    from paper_1909_00899_b200.align import PairsBatch
+
+    batch = PairsBatch(w.scheme, kernel=args.kernel, coords=False)
+    batch.upload(w.flat_q, w.q_off, w.flat_r, w.r_off)
+    coords_batch = PairsBatch(w.scheme, kernel=args.kernel, coords=True)
+    coords_batch.dev, coords_batch.n, coords_batch.qlen_rng = batch.dev, batch.n, batch.qlen_rng
+    coords_batch.out = coords_batch._outputs(batch.n)
+    torch.cuda.synchronize()
+    n = batch.n
+
+    def step():
+        return batch.run()
+
+    from paper_1909_00899_b200 import _lib
+    from paper_1909_00899_b200.align import _ptr, _stream
+
+    def kernel_only():
+        d, o, s = batch.dev, batch.out, batch.scheme
+        _lib.check(L.sw_pairs_align(16, 0, batch.kid, _ptr(d["q"]), _ptr(d["qs"]), _ptr(d["ql"]),
+                                     _ptr(d["t"]), _ptr(d["ts"]), _ptr(d["tl"]), None, n, None,
+                                     *batch.qlen_rng, _ptr(batch.sub), s.n_symbols, s.gap_open,
+                                     s.gap_extend, s.bias, s.max_score, None, None, None, None,
+                                     _ptr(o["score"]), None, None, _ptr(o["flags"]), None, None,
+                                     _stream()))
+
+    host = batch.pin_host(w.flat_q, w.q_off, w.flat_r, w.r_off)
+    e2e_batch = PairsBatch(w.scheme, kernel=args.kernel, coords=False)
+    e2e_batch.prepare_host(host, n_chunks=16)
+
+    def e2e_step():
+        out = e2e_batch.run_host(host)
+        torch.cuda.current_stream().synchronize()
+        return out
+
+    def variants():
+        res = {}
+        for name, b, fn in (("scan+coords", coords_batch, coords_batch.run),):
+            ms = timer.run(fn, max(2, args.steps // 2)) / max(2, args.steps // 2)
+            res[name] = {"ms": round(ms, 3), "gcups_rank": round(150 * 300 * n / ms / 1e6, 2)}
+        lz = PairsBatch(w.scheme, kernel="lazyf", coords=False)
+        lz.dev, lz.n, lz.qlen_rng, lz.out = batch.dev, n, batch.qlen_rng, lz._outputs(n)
+        ms = timer.run(lz.run, 1)
+        res["lazyf"] = {"ms": round(ms, 3), "gcups_rank": round(150 * 300 * n / ms / 1e6, 2)}
+        return res
+
+    # per pair: 450 residue bytes + q/t start (8+8) + q/t length (4+4) + score 4 + flags 1
+    alg_bytes = n * (450 + 24 + 5)
+    return {
+        "step": step, "kernel_only": kernel_only, "e2e_step": e2e_step, "engine": batch,
+        "rank_cells": 150 * 300 * n, "h2d": e2e_batch.h2d_bytes, "d2h": e2e_batch.d2h_bytes,
+        "kernel_name": "sw_striped_kernel<W16,T=4,L=19,SCAN,exact,ge=1> (pairs mode, score-only)",
+        "width": 16, "alg_bytes": alg_bytes, "traffic": None, "variants": variants,
+        "extra_config": {"lanes": 8, "seg_len": 19},
+        "result": lambda out: {"rank_score_sum": int(out["score"][:n].sum().item())},
+    }
+
+
+# ---- configs 1, 4, 5 (single pair) ----------------------------------------------------
+
+
+def device_single(cfg, args, w, rank, world, timer, L):
+    import ctypes as C
+
+    import torch
+
+    from paper_1909_00899_b200 import _lib, align
+    from paper_1909_00899_b200.align import _ptr, _stream
+
+    sch = w.scheme
+    q = torch.from_numpy(w.query).cuda()
+    r = torch.from_numpy(w.ref).cuda()
+    sub = torch.from_numpy(sch.as_array()).cuda()
+    m, n = int(q.numel()), int(r.numel())
+    out = torch.zeros(4, dtype=torch.int32, device="cuda")
+    fl = torch.zeros(1, dtype=torch.uint8, device="cuda")
+    o3 = (C.c_void_p(out.data_ptr()), C.c_void_p(out.data_ptr() + 4),
+          C.c_void_p(out.data_ptr() + 8))
+
+    def long_fn(kernel, width):
+        nbytes = int(L.sw_long_workspace_bytes(m, n, sch.n_symbols, width))
+        ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        kid = _lib.KERNEL_IDS[kernel]
+
+        def fn():
+            _lib.check(L.sw_align_long(width, kid, _ptr(q), m, _ptr(r), n, _ptr(sub),
+                                       sch.n_symbols, sch.gap_open, sch.gap_extend, sch.bias,
+                                       sch.max_score, _ptr(ws), nbytes, *o3, _ptr(fl), _stream()))
+        return fn
+
+    def warp_fn(kernel, lanes):
+        prof = align.build_profile_arrays(w.query, sch, lanes)
+        plan, pr = prof.for_kernel(kernel)
+        kid = _lib.KERNEL_IDS[kernel]
+        start = torch.zeros(1, dtype=torch.int64, device="cuda")
+        length = torch.full((1,), n, dtype=torch.int32, device="cuda")
+
+        def fn():
+            _lib.check(L.sw_db_align(C.byref(plan), _ptr(pr), kid, sch.gap_open, sch.gap_extend,
+                                     prof.bias, prof.max_sub, _ptr(r), _ptr(start), _ptr(length),
+                                     None, 1, None, *o3, _ptr(fl), None, None, None, _stream()))
+        return fn, f"warp kernel W16 P={plan.lanes} L={plan.seg_len}"
+
+    def block_fn(kernel, lanes, width):
+        kid = _lib.KERNEL_IDS[kernel]
+        geo = _lib.block_plan(m, sch.n_symbols, width, kid, lanes)
+
+        def fn():
+            _lib.check(L.sw_align_block(width, kid, geo[0], _ptr(q), m, _ptr(r), n, _ptr(sub),
+                                        sch.n_symbols, sch.gap_open, sch.gap_extend, sch.bias,
+                                        sch.max_score, 1, *o3, _ptr(fl), None, None, _stream()))
+        return fn, f"block kernel W{width} p={geo[0]} ({geo[1]} threads x {geo[2]} CTAs, L={geo[3]})"
+
+    if cfg == 1:
+        launches = 1  # sw_db_align: one striped-kernel launch
+        main_fn, main_desc = warp_fn("scan", 16)
+        variants_spec = [("lazyf", *warp_fn("lazyf", 16)),
+                         ("lazyf-noexit", *warp_fn("lazyf-noexit", 16)),
+                         ("scan-p64", *warp_fn("scan", 64)),
+                         ("lazyf-p64", *warp_fn("lazyf", 64)),
+                         ("wavefront", long_fn("wavefront", 32), "wavefront strips (sw_align_long)")]
+        e2e_call = lambda: align.align_pair("scan", 16, w.query, w.ref, sch)  # noqa: E731
+        kname = main_desc + " scan"
+    elif cfg == 4:
+        launches = 2  # sw_align_long: strip-profile kernel + cooperative strip kernel
+        main_fn, main_desc = long_fn("scan", 32), "scan strip pipeline W32 (sw_align_long)"
+        variants_spec = [("scan-block-p128", *block_fn("scan", 128, 32)),
+                         ("lazyf-block-p128", *block_fn("lazyf", 128, 32)),
+                         ("wavefront", long_fn("wavefront", 32), "wavefront strips W32")]
+        e2e_call = lambda: align.align_long(w.query, w.ref, sch, width=32)  # noqa: E731
+        kname = "sw_chain_kernel<W32> (scan strips)"
+    else:
+        launches = 2
+        main_fn, main_desc = long_fn("scan", 32), "scan strip pipeline W32 (sw_align_long)"
+        variants_spec = [("wavefront", long_fn("wavefront", 32), "wavefront strips W32")]
+        e2e_call = lambda: align.align_long(w.query, w.ref, sch, width=32)  # noqa: E731
+        kname = "sw_chain_kernel<W32> (scan strips)"
+
+    def step():
+        main_fn()
+        return out
+
+    def variants():
+        res = {}
+        for name, fn, desc in variants_spec:
+            steps = 1 if name.startswith("lazyf") and cfg == 4 else max(2, args.steps // 2)
+            fn()
+            torch.cuda.synchronize()
+            ms = timer.run(fn, steps) / steps
+            o = out.cpu().tolist()
+            res[name] = {"ms": round(ms, 4), "gcups": round(m * n / ms / 1e6, 3), "path": desc,
+                         "score": o[0], "ref_end": o[1], "query_end": o[2]}
+        return res
+
+    def e2e_step():
+        return e2e_call()
+
+    return {
+        "step": step, "kernel_only": main_fn, "e2e_step": e2e_step, "engine": None,
+        "rank_cells": m * n, "h2d": m + n + sch.n_symbols ** 2, "d2h": 16,
+        "kernel_name": kname, "width": 32 if cfg in (4, 5) else 16, "alg_bytes": m + n,
+        "traffic": None, "variants": variants, "extra_config": {"path": main_desc},
+        "result": lambda o: {"score": int(o[0].item()), "ref_end": int(o[1].item()),
+                             "query_end": int(o[2].item())},
+        "latency": {"columns": n}, "launches_per_step": launches,
+    }
 
 
 def main() -> None:
@@ -232,8 +805,9 @@ def main() -> None:
     import torch
     import torch.distributed as dist
 
-    from paper_1909_00899_b200 import _lib, search, workloads as W
+    from paper_1909_00899_b200 import _lib
 
+    cfg = args.config
     world, rank, local = dist_env()
     # SWB_DIST_BACKEND=gloo lets the multi-rank path run with several ranks on one
     # GPU (shards never wait on each other); the product path is NCCL, one rank per GPU.
@@ -250,175 +824,96 @@ def main() -> None:
         if world > 1:
             dist.barrier()
 
-    w = W.config2(n_targets=args.n_targets)
-    m = int(w.query.shape[0])
-    ids = search.shard(w.offsets, rank, world)
-    packed = search.pack(w.db, w.offsets, ids)
-    total_cells = m * int(w.offsets[-1])
-    rank_cells = m * packed.residues
-
-    eng = search.DatabaseSearch(w.scheme, kernel=args.kernel, coords="topk", k=TOPK)
-    eng.upload(packed)
-    eng.set_query(w.query)
-    torch.cuda.synchronize()
+    L = _lib.load()
     stream = torch.cuda.current_stream()
-
-    def step():
-        eng.rebuild_profile()
-        eng.align()
-        top = eng.topk(TOPK)
-        return search.merge_topk(top, TOPK)
+    w = load_workload(cfg, args, rank, world)
+    timer = Timer(stream, world, backend, flush=cfg in (1, 4, 5))
+    if cfg == 2:
+        d = device_config2(args, w, rank, world, timer, L)
+    elif cfg == 3:
+        d = device_config3(args, w, rank, world, timer, L)
+    else:
+        d = device_single(cfg, args, w, rank, world, timer, L)
+    cells = total_cells(cfg, w, args) * (world if cfg in (1, 4, 5) else 1)
+    eng = d["engine"]
 
     sampler = ClockSampler(local)
     sampler.start()
     for _ in range(max(3, args.warmup)):
-        step()
+        d["step"]()
     torch.cuda.synchronize()
 
     # ---- value: device-resident inputs, whole step, max over ranks ----
-    launches0 = eng.launches
+    launches0 = eng.launches if eng is not None else 0
     sampler.mark()
     barrier()
     torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        top = step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
+    ms = timer.run(d["step"], args.steps)
     barrier()
     clocks = sampler.stop()
-    ms = ev0.elapsed_time(ev1)
-    gpu_launches = eng.launches - launches0
-    if world > 1:
-        t = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    last = timer.last
+    gpu_launches = ((eng.launches - launches0) if eng is not None
+                    else args.steps * d["launches_per_step"])
     ms_step = ms / args.steps
-    value = total_cells / (ms_step * 1e-3) / 1e9
+    value = cells / (ms_step * 1e-3) / 1e9
 
-    # ---- dominant kernel alone: 16-bit striped kernel, events on its stream ----
-    L = _lib.load()
-    import ctypes as C
-
-    from paper_1909_00899_b200.align import _ptr, _stream
-
-    p, d, o = eng.prof, eng.dev, eng.out
+    # ---- dominant kernel alone ----
     k_reps = max(3, args.steps)
-    ek0, ek1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ek0.record(stream)
-    for _ in range(k_reps):
-        _lib.check(L.sw_db_align(C.byref(eng.plan16), _ptr(eng.prof16), eng.kid, w.scheme.gap_open,
-                                 w.scheme.gap_extend, p.bias, p.max_sub, _ptr(d.codes),
-                                 _ptr(d.start), _ptr(d.length), None, d.n, None,
-                                 _ptr(o["score"]), _ptr(o["ref_end"]), _ptr(o["query_end"]),
-                                 _ptr(o["flags"]), None, None, C.byref(_lib.DbOpts(d_coord_floor=o["_floor"].data_ptr())), _stream()))
-    ek1.record(stream)
-    torch.cuda.synchronize()
-    k_ms = ek0.elapsed_time(ek1) / k_reps
-    kernel_gcups = rank_cells / (k_ms * 1e-3) / 1e9
+    k_ms = timer.run(d["kernel_only"], k_reps) / k_reps
+    kernel_gcups = d["rank_cells"] / (k_ms * 1e-3) / 1e9
+    peaks = dpx_peaks(L, stream)
+    peak = peaks["peak16_gcups"] if d["width"] == 16 else peaks["peak32_gcups"]
+    variants = d["variants"]() if "variants" in d else None
 
-    # ---- DPX issue peak (measured live): cell-update instruction mix ----
-    scratch = torch.zeros(256, dtype=torch.int32, device="cuda")
-    L.sw_dpx_probe(1, 1000, _ptr(scratch), _stream())
-    torch.cuda.synchronize()
-    iters = 20000
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    n_instr = L.sw_dpx_probe(1, iters, _ptr(scratch), _stream())
-    e1.record(stream)
-    torch.cuda.synchronize()
-    dpx_instr_per_s = n_instr / (e0.elapsed_time(e1) * 1e-3)
-    e0.record(stream)
-    n0 = L.sw_dpx_probe(0, iters, _ptr(scratch), _stream())
-    e1.record(stream)
-    torch.cuda.synchronize()
-    viaddmnmx_per_s = n0 / (e0.elapsed_time(e1) * 1e-3)
-    # algorithmic minimum: 6 lane-instructions per cell, 2 cells per 16x2 instruction
-    peak_gcups = dpx_instr_per_s * 2 / 6 / 1e9
-
-    # ---- e2e: public API with host buffers (H2D of the shard + D2H of the top-k) ----
-    # what search_streamed copies per step: residues, starts, lengths, ids (the
-    # processing order is the identity for a length-sorted pack and stays on the
-    # device) + the query
-    h2d = sum(int(t.numel() * t.element_size())
-              for t in (packed.codes, packed.start, packed.length, packed.ids)) + m
-    d2h = TOPK * 4 * 8
-
-    # under a profiler (ncu injects itself through CUDA_INJECTION64_PATH) kernels are
-    # serialised, so a launch waiting on chunks a concurrent copy delivers would
-    # never see them: upload first, then search
-    profiled = "CUDA_INJECTION64_PATH" in os.environ
-
-    def e2e_step():
-        eng.set_query(w.query)
-        if profiled:
-            eng.upload(packed)
-            eng.align()
-        else:
-            eng.search_streamed(packed, n_chunks=64)  # one launch; tasks wait for their chunk
-        return search.merge_topk(eng.topk(TOPK), TOPK).cpu()
-
+    # ---- e2e: public API with host buffers ----
     for _ in range(max(3, args.warmup)):
-        e2e_step()
+        d["e2e_step"]()
     barrier()
     torch.cuda.synchronize()
+    t0 = time.perf_counter()
     ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ee0.record(stream)
     for _ in range(args.steps):
-        host_top = e2e_step()
+        d["e2e_step"]()
     ee1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = ee0.elapsed_time(ee1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda" if backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = total_cells / (e2e_ms / args.steps * 1e-3) / 1e9
+    e2e_ms = max(ee0.elapsed_time(ee1), (time.perf_counter() - t0) * 1e3)
+    e2e_ms = timer.max_over_ranks(e2e_ms)
+    e2e_value = cells / (e2e_ms / args.steps * 1e-3) / 1e9
 
     if rank == 0:
-        mp = {}
-        try:
-            with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
-                mp = json.load(fh)
-        except OSError:
-            pass
-        hbm_peak = float(mp.get("hbm_gbs", 6650.0))
-        alg_bytes = packed.residues + d.n * (8 + 4 + 4 + 4 + 4 + 4 + 1)  # residues + per-target I/O
-        hbm_achieved = alg_bytes / (k_ms * 1e-3) / 1e9
+        hbm = hbm_peak()
+        hbm_achieved = d["alg_bytes"] / (k_ms * 1e-3) / 1e9
+        roof = {"bound": "dpx", "achieved": round(kernel_gcups, 3), "peak": round(peak, 2),
+                "unit": "GCUPS", "frac": round(kernel_gcups / peak, 5),
+                "traffic": d["traffic"], "kernel": d["kernel_name"], "kernel_ms": round(k_ms, 4),
+                "peak_source": ("live DPX probe (cell-update mix; 6 lane-instructions per cell, "
+                                f"{'2 cells per 16x2 instruction' if d['width'] == 16 else '1 cell per 32-bit instruction'})"),
+                "dpx_probe": {k: peaks[k] for k in ("mix_instr_per_s", "viaddmnmx_s16x2_instr_per_s")},
+                "hbm": {"achieved": round(hbm_achieved, 3), "peak": hbm, "unit": "GB/s",
+                        "frac": round(hbm_achieved / hbm, 6), "algorithmic_bytes": int(d["alg_bytes"])}}
+        if "latency" in d:
+            cols = d["latency"]["columns"]
+            roof["latency"] = {"columns": cols, "ns_per_column": round(k_ms * 1e6 / cols, 2),
+                               "note": "single pair: n dependent reference columns"}
         line = {
-            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "s16x2",
-            "data": "synthetic",
-            "config": {**arm_config(w, args, world), "lanes": eng.plan16.lanes,
-                       "seg_len": eng.plan16.seg_len,
-                       "end_coords": "exact for every target scoring >= the in-kernel floor "
-                                     "(k-th best of a strided 1/16 sample: a superset of the "
-                                     "top-k); others score-only"},
-            "roofline": {"bound": "dpx", "achieved": round(kernel_gcups, 2),
-                         "peak": round(peak_gcups, 2), "unit": "GCUPS",
-                         "frac": round(kernel_gcups / peak_gcups, 4),
-                         # dram__bytes_read+write per launch of this kernel (one ncu --set
-                         # full capture at this config, profiles/r01i_config2_db_kernel.md)
-                         "traffic": 509.05e6,
-                         "kernel": (f"sw_striped_kernel<W16,T={eng.plan16.threads},"
-                                    f"L={eng.plan16.seg_len},{args.kernel.upper()},ge={w.scheme.gap_extend}>"),
-                         "kernel_ms": round(k_ms, 3),
-                         "peak_source": "live DPX probe (cell-update mix, 6 instr per 2 cells)",
-                         "dpx_probe": {"mix_instr_per_s": dpx_instr_per_s,
-                                       "viaddmnmx_s16x2_instr_per_s": viaddmnmx_per_s},
-                         "hbm": {"achieved": round(hbm_achieved, 2), "peak": hbm_peak,
-                                 "unit": "GB/s", "frac": round(hbm_achieved / hbm_peak, 5),
-                                 "algorithmic_bytes": int(alg_bytes)}},
-            "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h)},
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True,
+            "scaling": "weak" if cfg in (1, 4, 5) else "strong", "vs_baseline": None,
+            "dtype": CONFIGS[cfg]["dtype"], "data": "synthetic",
+            "config": {**arm_config(cfg, w, args, world), **d["extra_config"]},
+            "roofline": roof,
+            "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": int(d["h2d"]),
+                    "d2h_bytes_per_step": int(d["d2h"])},
             "gpu_launches": int(gpu_launches),
             "clocks": clocks,
-            "top_hit": [int(x) for x in host_top[0].tolist()],
+            **d["result"](last),
         }
+        if variants:
+            line["variants"] = variants
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
+            line["cpu_baseline"] = cpu_baseline(cfg, w, args.cpu_seconds)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -757,3 +757,149 @@ def scan_lanes(f, d, width: int = 32) -> np.ndarray:
     out = torch.empty_like(fd)
     _lib.check(_lib.load().sw_scan_lanes(width, p, _ptr(fd), _ptr(dd), n, _ptr(out), _stream()))
     return out.cpu().numpy().view(np.uint16)
+
+
+class PairsBatch:
+    """Device form of ``batch_align`` for large batches of one scheme (config 3):
+    the reference's serial pair loop (src/_compiled.py:504-529) becomes one
+    striped-kernel launch over every pair (per-pair profiles built inside the
+    kernel) plus a device-counted 32-bit re-run of the rare 16-bit wrap-guard hits.
+
+    ``upload(...)`` makes the batch device-resident (``run`` then times the
+    alignment alone); ``run_host(...)`` is the end-to-end form for pinned host
+    buffers: chunks are copied on a copy stream while the previous chunk is
+    aligned, and the scores (and coordinates) come back per chunk. Results are
+    exact either way (tests/test_gpu_fullsize.py)."""
+
+    def __init__(self, scheme: ScoringScheme, kernel: str = "scan", coords: bool = False,
+                 lanes: int = 0):
+        self.scheme = as_scheme(scheme)
+        self.kernel = kernel
+        self.kid = _kernel_id(kernel)
+        self.coords = coords
+        self.lanes = lanes
+        self.launches = 0
+        self.sub = None
+
+    def _meta(self, q_off, r_off):
+        q_off = np.asarray(q_off, dtype=np.int64)
+        r_off = np.asarray(r_off, dtype=np.int64)
+        return (q_off[:-1], np.diff(q_off).astype(np.int32), r_off[:-1],
+                np.diff(r_off).astype(np.int32))
+
+    def upload(self, flat_q, q_off, flat_r, r_off) -> None:
+        """Copy a CSR batch to the device (outside any timed region)."""
+        _require_cuda()
+        qs, ql, ts, tl = self._meta(q_off, r_off)
+        n = int(ql.shape[0])
+        self.n = n
+        self.qlen_rng = (int(ql.min()) if n else 0, int(ql.max()) if n else 0)
+        f = lambda a, dt=None: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        self.dev = {"q": f(_codes(flat_q, self.scheme.n_symbols, "query")), "qs": f(qs),
+                    "ql": f(ql), "t": f(_codes(flat_r, self.scheme.n_symbols, "reference")),
+                    "ts": f(ts), "tl": f(tl)}
+        self.out = self._outputs(n)
+
+    def _outputs(self, n: int) -> dict:
+        o = {k: torch.zeros(max(n, 1), dtype=torch.int32, device="cuda")
+             for k in ("score", "ref_end", "query_end")}
+        o["flags"] = torch.zeros(max(n, 1), dtype=torch.uint8, device="cuda")
+        o["_list"] = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        o["_cnt"] = torch.zeros(1, dtype=torch.int64, device="cuda")
+        return o
+
+    def _launch(self, dev: dict, out: dict, n: int, qmin: int, qmax: int) -> None:
+        L = _lib.load()
+        sch = self.scheme
+        if self.sub is None:
+            self.sub = torch.from_numpy(sch.as_array()).cuda()
+        st = _stream()
+        co = self.coords
+        args = (_ptr(dev["q"]), _ptr(dev["qs"]), _ptr(dev["ql"]), _ptr(dev["t"]), _ptr(dev["ts"]),
+                _ptr(dev["tl"]))
+        tail = (_ptr(self.sub), sch.n_symbols, sch.gap_open, sch.gap_extend, sch.bias,
+                sch.max_score, None, None, None, None, _ptr(out["score"]),
+                _ptr(out["ref_end"]) if co else None, _ptr(out["query_end"]) if co else None,
+                _ptr(out["flags"]), None, None, st)
+        _lib.check(L.sw_pairs_align(16, self.lanes, self.kid, *args, None, n, None, qmin, qmax,
+                                    *tail))
+        # 16-bit wrap-guard hits: collected and re-run in 32 bits on the device
+        _lib.check(L.sw_collect_flagged(_ptr(out["flags"]), n, _lib.FLAG_RESCUE,
+                                        _ptr(out["_list"]), _ptr(out["_cnt"]), st))
+        _lib.check(L.sw_pairs_align(32, 0, self.kid, *args, _ptr(out["_list"]), 0,
+                                    _ptr(out["_cnt"]), 0, qmax, *tail))
+        self.launches += 3
+
+    def run(self) -> dict:
+        """Align the uploaded batch; device results (score, ref_end, query_end, flags)."""
+        self._launch(self.dev, self.out, self.n, *self.qlen_rng)
+        return self.out
+
+    @staticmethod
+    def pin_host(flat_q, q_off, flat_r, r_off) -> dict:
+        """Pinned host copies of a CSR batch (the e2e input form)."""
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        return {"q": pin(np.asarray(flat_q, np.uint8)), "q_off": np.asarray(q_off, np.int64),
+                "t": pin(np.asarray(flat_r, np.uint8)), "r_off": np.asarray(r_off, np.int64)}
+
+    def prepare_host(self, host: dict, n_chunks: int = 16) -> None:
+        """Per-chunk metadata (chunk-relative starts, lengths) in pinned memory and
+        double-buffered device chunk buffers; done once per batch, outside timing."""
+        q_off, r_off = host["q_off"], host["r_off"]
+        n = int(q_off.shape[0] - 1)
+        n_chunks = max(1, min(n_chunks, n))
+        bounds = [n * c // n_chunks for c in range(n_chunks + 1)]
+        chunks = []
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            qs = q_off[a:b] - q_off[a]
+            ts = r_off[a:b] - r_off[a]
+            meta = torch.from_numpy(np.concatenate([
+                qs.view(np.int32), ts.view(np.int32), np.diff(q_off[a:b + 1]).astype(np.int32),
+                np.diff(r_off[a:b + 1]).astype(np.int32)])).pin_memory()
+            ql = np.diff(q_off[a:b + 1])
+            chunks.append((a, b, int(q_off[a]), int(q_off[b]), int(r_off[a]), int(r_off[b]), meta,
+                           int(ql.min()) if b > a else 0, int(ql.max()) if b > a else 0))
+        self.chunks = chunks
+        mq = max(c[3] - c[2] for c in chunks)
+        mt = max(c[5] - c[4] for c in chunks)
+        mn = max(c[1] - c[0] for c in chunks)
+        self.bufs = [{"q": torch.empty(max(mq, 1), dtype=torch.uint8, device="cuda"),
+                      "t": torch.empty(max(mt, 1), dtype=torch.uint8, device="cuda"),
+                      "meta": torch.empty(6 * mn, dtype=torch.int32, device="cuda"),
+                      "out": self._outputs(mn)} for _ in range(2)]
+        self.host_out = {k: torch.empty(n, dtype=torch.int32).pin_memory()
+                         for k in (("score", "ref_end", "query_end") if self.coords else ("score",))}
+        self.host_out["flags"] = torch.empty(n, dtype=torch.uint8).pin_memory()
+        self.copy_stream = torch.cuda.Stream()
+        self.h2d_bytes = int(host["q"].numel() + host["t"].numel()
+                             + sum(c[6].numel() * 4 for c in chunks))
+        self.d2h_bytes = int(sum(v.numel() * v.element_size() for v in self.host_out.values()))
+
+    def run_host(self, host: dict) -> dict:
+        """End to end from pinned host buffers: chunk c+1 is copied while chunk c is
+        aligned; per-chunk results are copied back into pinned host arrays. Returns
+        the host result tensors (valid after a synchronize)."""
+        cur = torch.cuda.current_stream()
+        cp = self.copy_stream
+        ready = [torch.cuda.Event() for _ in self.chunks]
+        freed = [torch.cuda.Event() for _ in range(2)]
+        for c, (a, b, qa, qb, ta, tb, meta, qmin, qmax) in enumerate(self.chunks):
+            buf = self.bufs[c & 1]
+            n = b - a
+            with torch.cuda.stream(cp):
+                if c >= 2:
+                    cp.wait_event(freed[c & 1])  # the chunk that used this buffer is done
+                buf["q"][: qb - qa].copy_(host["q"][qa:qb], non_blocking=True)
+                buf["t"][: tb - ta].copy_(host["t"][ta:tb], non_blocking=True)
+                buf["meta"][: 6 * n].copy_(meta, non_blocking=True)
+                ready[c].record(cp)
+            cur.wait_event(ready[c])
+            m = buf["meta"]
+            dev = {"q": buf["q"], "t": buf["t"], "qs": m[0:2 * n], "ts": m[2 * n:4 * n],
+                   "ql": m[4 * n:5 * n], "tl": m[5 * n:6 * n]}
+            o = buf["out"]
+            self._launch(dev, o, n, qmin, qmax)
+            for k, v in self.host_out.items():
+                v[a:b].copy_(o[k][:n], non_blocking=True)
+            freed[c & 1].record(cur)
+        return self.host_out

@@ -195,20 +195,23 @@ C3_CHUNK = 1 << 16  # config 3 pairs per independently seeded generator block
 
 
 def config3(n_pairs: int = 1 << 24, seed: int = SEEDS[3], start: int = 0,
-            stop: int | None = None) -> BatchWorkload:
+            stop: int | None = None, threads: int = 0) -> BatchWorkload:
     """Short reads: 150 nt read vs 300 nt window, 1% subs, 0.1% indels (1..3).
 
     Pairs are generated in blocks of C3_CHUNK, block b from its own generator
     ``default_rng((seed, b))``, so any pair range [start, stop) -- a rank's shard
     -- is generated without the pairs before it, and a smaller n_pairs is a prefix
     of the full batch. Returns the pairs [start, stop) (default: all n_pairs)."""
+    import os
+
+    threads = threads or min(8, os.cpu_count() or 1)
     stop = n_pairs if stop is None else min(stop, n_pairs)
     start = max(0, min(start, stop))
     W, R = 300, 150
     n_out = stop - start
     flat_r = np.empty(n_out * W, dtype=np.uint8)
     flat_q = np.empty(n_out * R, dtype=np.uint8)
-    for blk in range(start // C3_CHUNK, -(-stop // C3_CHUNK)):
+    def make_block(blk: int) -> None:
         rng = np.random.default_rng((seed, blk))
         b0 = blk * C3_CHUNK
         n = min(C3_CHUNK, n_pairs - b0)
@@ -238,6 +241,16 @@ def config3(n_pairs: int = 1 << 24, seed: int = SEEDS[3], start: int = 0,
         a, b = max(start, b0), min(stop, b0 + n)  # the part of this block in [start, stop)
         flat_r[(a - start) * W:(b - start) * W] = win[a - b0:b - b0].reshape(-1)
         flat_q[(a - start) * R:(b - start) * R] = read[a - b0:b - b0].reshape(-1)
+
+    blocks = range(start // C3_CHUNK, -(-stop // C3_CHUNK))
+    if threads > 1 and len(blocks) > 1:  # blocks are independent; numpy releases the GIL
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(min(threads, len(blocks))) as ex:
+            list(ex.map(make_block, blocks))
+    else:
+        for blk in blocks:
+            make_block(blk)
     q_off = np.arange(n_out + 1, dtype=np.int64) * R
     r_off = np.arange(n_out + 1, dtype=np.int64) * W
     scheme = ScoringScheme.match_mismatch(DNA4, 2, -4, 6, 1)

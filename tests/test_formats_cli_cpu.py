@@ -117,3 +117,108 @@ def test_shard_pairs_partition():
             assert parts[0][0] == 0 and parts[-1][1] == n
             assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
             assert max(b - a for a, b in parts) - min(b - a for a, b in parts) <= 1
+
+
+def _reference_formats():
+    import importlib
+    import os
+    import sys
+
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline",
+                       "_ref")
+    if not os.path.isdir(os.path.join(ref, "swscan")):
+        pytest.skip("reference package not installed in baseline/_ref")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/swscan_numba_cache")
+    return importlib.import_module("swscan.formats"), importlib.import_module("swscan.scoring")
+
+
+def _random_fasta(rng) -> bytes:
+    pieces = [b">", b"> ", b">id", b">id desc", b">a  b c ", b"\n", b"\r\n", b"\r", b"\x0b",
+              b"\x0c", b"\x1c", b"  ", b"\t", b"\x1f", b"ACGT", b"acgt", b"N", b"AC GT", b"X",
+              b"-", b"*", b"GATTACA", b"gg", b">q1", b">q2 x"]
+    k = int(rng.integers(0, 14))
+    return b"".join(pieces[int(i)] for i in rng.integers(0, len(pieces), k))
+
+
+def test_read_fasta_slices_agree(monkeypatch):
+    """The threaded byte passes (buffer cut at line breaks) give the single-slice result."""
+    rng = np.random.default_rng(0x511CE)
+    data = b"".join(_random_fasta(rng) for _ in range(3000)) + b"\n>z\nACGT\n"
+    data = b">a\n" + data.replace(b">\n", b">x\n").replace(b"> \n", b">y\n")
+    try:
+        one = formats.read_fasta(data, None, threads=1)
+        want = (one.ids, one.descriptions, one.codes.tolist(), one.offsets.tolist())
+    except formats.MalformedFasta as e:
+        want = str(e)
+    monkeypatch.setattr(formats, "_MIN_SPLIT", 1)
+    for t in (2, 3, 7, 16):
+        try:
+            b = formats.read_fasta(data, None, threads=t)
+            got = (b.ids, b.descriptions, b.codes.tolist(), b.offsets.tolist())
+        except formats.MalformedFasta as e:
+            got = str(e)
+        assert got == want, t
+
+
+def test_parse_fasta_differential_vs_reference():
+    """The byte-level ingester against the reference's line parser on 4,000 random
+    inputs built from FASTA's corner cases: identical records, or the same
+    MalformedFasta message (the first problem the reference meets)."""
+    ref_formats, ref_scoring = _reference_formats()
+    rng = np.random.default_rng(0xFA57A)
+    for i in range(4000):
+        data = _random_fasta(rng)
+        for alph in (None, "dna"):
+            a_ref = ref_scoring.Alphabet.dna() if alph else None
+            a_new = Alphabet.dna() if alph else None
+            try:
+                want = [(r.id, r.description, r.sequence) for r in
+                        ref_formats.parse_fasta(data, a_ref)]
+            except ref_formats.MalformedFasta as e:
+                want = ("error", str(e))
+            try:
+                got = [(r.id, r.description, r.sequence) for r in formats.parse_fasta(data, a_new)]
+            except formats.MalformedFasta as e:
+                got = ("error", str(e))
+            assert got == want, (i, data, alph)
+            if alph and not isinstance(want, tuple):
+                b = formats.read_fasta(data, a_new)
+                codes = [list(a_new.lut()[np.frombuffer(s.encode(), np.uint8)]) for _, _, s in want]
+                assert [b.codes[b.offsets[j]:b.offsets[j + 1]].tolist() for j in range(len(b))] == codes
+    # non-ASCII bytes: same error class and message as the reference's decode
+    for bad in (b">a\nAC\xff\n", b"\x80"):
+        with pytest.raises(ref_formats.MalformedFasta) as e1:
+            ref_formats.parse_fasta(bad)
+        with pytest.raises(formats.MalformedFasta) as e2:
+            formats.parse_fasta(bad)
+        assert str(e1.value) == str(e2.value)
+
+
+def test_read_fasta_million_records_is_vectorised():
+    """1,000,000 records (~30M residues) parse and encode in a few seconds."""
+    import time
+
+    rng = np.random.default_rng(5)
+    lens = rng.integers(10, 50, 1_000_000)
+    body = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, int(lens.sum()))]
+    lines = []
+    o = 0
+    for i, ln in enumerate(lens[:1000]):  # a hand-made prefix for the content check
+        lines.append(b">r%d d\n" % i + body[o:o + ln].tobytes() + b"\n")
+        o += ln
+    # the rest assembled in bulk (header + sequence per record)
+    hdr = np.char.add(np.char.add(">r", np.arange(1000, 1_000_000).astype(str)), " d\n")
+    seqs = np.split(body[o:], np.cumsum(lens[1000:])[:-1])
+    rest = b"".join(h.encode() + s.tobytes() + b"\n" for h, s in zip(hdr, seqs))
+    data = b"".join(lines) + rest
+    t0 = time.perf_counter()
+    b = formats.read_fasta(data, Alphabet("ACGT"))
+    dt = time.perf_counter() - t0
+    assert len(b) == 1_000_000 and (b.lengths == lens).all()
+    assert b.ids[12345] == "r12345" and b.descriptions[7] == "d"
+    lut = Alphabet("ACGT").lut()
+    assert (b.codes[: lens[0]] == lut[body[: lens[0]]]).all()
+    assert (b.codes[-lens[-1]:] == lut[body[-lens[-1]:]]).all()
+    assert dt < 20.0, dt

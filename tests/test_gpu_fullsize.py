@@ -1,0 +1,127 @@
+"""Full-size parity: every output of configs 2, 3 and 5 against the CPU oracle.
+
+tests/golden/fullsize.json holds the oracle's (score, ref_end, query_end) for
+all 1,000,000 config-2 targets, all 16,777,216 config-3 pairs and the config-5
+pair as digests (tests/golden/make_fullsize.py; oracle = _sw_scalar_c,
+src/_compiled.py:76-115, + first-maximum end coordinates). The inputs are
+regenerated here from their seeds and pinned by sha256. Both the scan (Alg. 6)
+and the lazy-F variants must reproduce the digests bit for bit, through the
+all-coordinates path and (config 2) the bench's coords="topk" path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from helpers import digest_mismatch, golden, result_digest, sha
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def A():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1909_00899_b200 import align
+
+    return align
+
+
+@pytest.fixture(scope="module")
+def G():
+    return golden("fullsize.json")
+
+
+@pytest.fixture(scope="module")
+def c2():
+    from paper_1909_00899_b200 import search, workloads as W
+
+    w = W.config2()
+    return w, search.pack(w.db, w.offsets, pin=False)
+
+
+@pytest.mark.parametrize("kernel", ["scan", "lazyf"])
+def test_config2_full_database_vs_oracle(A, G, c2, kernel):
+    from paper_1909_00899_b200 import search
+
+    w, packed = c2
+    want = G["config2"]
+    assert sha(w.query, w.db, w.offsets) == want["inputs_sha256"]
+    eng = search.DatabaseSearch(w.scheme, kernel=kernel, coords="all")
+    eng.upload(packed)
+    eng.set_query(w.query)
+    o = eng.align()
+    ids = eng.dev.ids.cpu().numpy()
+    n = w.n_targets
+    got = {}
+    for k in ("score", "ref_end", "query_end"):
+        a = np.empty(n, np.int32)
+        a[ids] = o[k][:n].cpu().numpy()
+        got[k] = a
+    d = result_digest(got["score"], got["ref_end"], got["query_end"], want["blocks"])
+    assert not digest_mismatch(d, want), digest_mismatch(d, want)
+    top = eng.topk(100).cpu().numpy()
+    assert top.tolist() == want["top100"]
+
+
+def test_config2_bench_path_topk_vs_oracle(A, G, c2):
+    """The bench step (coords='topk': in-kernel floor, located top hits) and the
+    streamed end-to-end form both return the oracle's top-100 records."""
+    from paper_1909_00899_b200 import search
+
+    w, packed = c2
+    eng = search.DatabaseSearch(w.scheme, coords="topk", k=100)
+    eng.upload(packed)
+    eng.set_query(w.query)
+    eng.align()
+    assert eng.topk(100).cpu().numpy().tolist() == G["config2"]["top100"]
+    eng2 = search.DatabaseSearch(w.scheme, coords="topk", k=100)
+    eng2.set_query(w.query)
+    eng2.search_streamed(search.pack(w.db, w.offsets), n_chunks=64)
+    assert eng2.topk(100).cpu().numpy().tolist() == G["config2"]["top100"]
+
+
+@pytest.fixture(scope="module")
+def c3():
+    from paper_1909_00899_b200 import workloads as W
+
+    return W.config3()
+
+
+@pytest.mark.parametrize("kernel", ["scan", "lazyf"])
+def test_config3_all_pairs_vs_oracle(A, G, c3, kernel):
+    w = c3
+    want = G["config3"]
+    assert sha(w.flat_q, w.flat_r) == want["inputs_sha256"]
+    r = A.pairs_align(w.flat_q, w.q_off, w.flat_r, w.r_off, kernel=kernel, scheme=w.scheme)
+    d = result_digest(r["score"], r["ref_end"], r["query_end"], want["blocks"])
+    assert not digest_mismatch(d, want), digest_mismatch(d, want)
+
+
+def test_config3_score_only_vs_oracle(A, G, c3):
+    """The metric's score-only launch (no end-coordinate search): every score equals
+    the all-coordinates run's, and the score sum and maximum equal the oracle's."""
+    w = c3
+    r = A.pairs_align(w.flat_q, w.q_off, w.flat_r, w.r_off, scheme=w.scheme, coords=False)
+    assert int(r["score"].sum()) == G["config3"]["score_sum"]
+    assert int(r["score"].max()) == G["config3"]["score_max"]
+    full = A.pairs_align(w.flat_q, w.q_off, w.flat_r, w.r_off, scheme=w.scheme)
+    assert (r["score"] == full["score"]).all()
+
+
+@pytest.mark.parametrize("kernel", ["scan", "wavefront"])
+def test_config5_full_pair_vs_oracle(A, G, kernel):
+    from paper_1909_00899_b200 import workloads as W
+
+    w = W.config5()
+    want = G["config5"]
+    assert sha(w.query, w.ref) == want["inputs_sha256"]
+    r = A.align_long(w.query, w.ref, w.scheme, width=32, kernel=kernel)
+    assert (r["score"], r["ref_end"], r["query_end"]) == (want["score"], want["ref_end"],
+                                                          want["query_end"])
+    g = golden("configs.npz")
+    if "c5_scan_p64_score" in g.files:  # the reference's own scan kernel agrees
+        assert want["score"] == int(g["c5_scan_p64_score"])

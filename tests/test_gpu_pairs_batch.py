@@ -1,0 +1,79 @@
+"""PairsBatch (config 3's device batch): resident and streamed-from-host forms
+against the oracle (batch_align / batch_oracle_scores, src/_compiled.py:491-529)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def A():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1909_00899_b200 import align
+
+    return align
+
+
+@pytest.mark.parametrize("coords", [False, True])
+def test_pairs_batch_resident_and_streamed(A, oracle, coords):
+    from paper_1909_00899_b200 import workloads as W
+
+    w = W.config3(n_pairs=50_000)
+    s, re_, qe = oracle.batch_scalar(w.flat_q, w.q_off, w.flat_r, w.r_off,
+                                     sub=w.scheme.as_array(), go=6, ge=1)
+    b = A.PairsBatch(w.scheme, coords=coords)
+    b.upload(w.flat_q, w.q_off, w.flat_r, w.r_off)
+    o = b.run()
+    assert (o["score"][: w.n_pairs].cpu().numpy() == s).all()
+    if coords:
+        assert (o["ref_end"][: w.n_pairs].cpu().numpy() == re_).all()
+        assert (o["query_end"][: w.n_pairs].cpu().numpy() == qe).all()
+    host = A.PairsBatch.pin_host(w.flat_q, w.q_off, w.flat_r, w.r_off)
+    e = A.PairsBatch(w.scheme, coords=coords)
+    e.prepare_host(host, n_chunks=7)
+    for _ in range(2):  # buffers are reused across calls
+        h = e.run_host(host)
+        torch.cuda.synchronize()
+        assert (h["score"].numpy() == s).all()
+        if coords:
+            assert (h["ref_end"].numpy() == re_).all() and (h["query_end"].numpy() == qe).all()
+
+
+def test_pairs_batch_mixed_lengths_and_rescue(A, oracle):
+    """Ragged pairs (empty, 1-residue, up to 300) and a scheme whose scores pass the
+    16-bit guard (re-run in 32 bits on the device), resident and streamed."""
+    from paper_1909_00899_b200.scoring import ScoringScheme
+
+    rng = np.random.default_rng(0x9A1)
+    n = 3000
+    ql = rng.integers(0, 300, n)
+    tl = rng.integers(0, 400, n)
+    ql[:5] = [0, 1, 300, 299, 0]
+    tl[:5] = [10, 0, 400, 1, 0]
+    q_off = np.concatenate([[0], np.cumsum(ql)]).astype(np.int64)
+    r_off = np.concatenate([[0], np.cumsum(tl)]).astype(np.int64)
+    fq = rng.integers(0, 4, q_off[-1]).astype(np.uint8)
+    fr = rng.integers(0, 4, r_off[-1]).astype(np.uint8)
+    fr[r_off[10]:r_off[10] + min(tl[10], ql[10])] = fq[q_off[10]:q_off[10] + min(tl[10], ql[10])]
+    mat = np.full((4, 4), -3, np.int8)
+    np.fill_diagonal(mat, 120)
+    sch = ScoringScheme.from_array(mat, 5, 2)
+    s, re_, qe = oracle.batch_scalar(fq, q_off, fr, r_off, sub=mat, go=5, ge=2)
+    assert s.max() > 32767 - 120  # some pairs need the 32-bit rescue
+    b = A.PairsBatch(sch, coords=True)
+    b.upload(fq, q_off, fr, r_off)
+    o = b.run()
+    assert (o["score"][:n].cpu().numpy() == s).all()
+    assert (o["ref_end"][:n].cpu().numpy() == re_).all()
+    host = A.PairsBatch.pin_host(fq, q_off, fr, r_off)
+    e = A.PairsBatch(sch, coords=True)
+    e.prepare_host(host, n_chunks=5)
+    h = e.run_host(host)
+    torch.cuda.synchronize()
+    assert (h["score"].numpy() == s).all() and (h["query_end"].numpy() == qe).all()
