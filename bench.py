@@ -620,7 +620,8 @@ def device_config2(args, w, rank, world, timer, L):
                          "end_coords": "exact for every target scoring >= the in-kernel floor "
                                        "(k-th best of a strided 1/16 sample: a superset of the "
                                        "top-k); others score-only"},
-        "result": lambda out: {"top_hit": [int(x) for x in out[0].tolist()]},
+        "result": lambda out: {"top_hit": [int(x) for x in out[0].tolist()],
+                               "topk_sha256": _sha(out.cpu().numpy())},
     }
 
 
@@ -683,8 +684,23 @@ def device_config3(args, w, rank, world, timer, L):
         "kernel_name": "sw_striped_kernel<W16,T=4,L=19,SCAN,exact,ge=1> (pairs mode, score-only)",
         "width": 16, "alg_bytes": alg_bytes, "traffic": None, "variants": variants,
         "extra_config": {"lanes": 8, "seg_len": 19},
-        "result": lambda out: {"rank_score_sum": int(out["score"][:n].sum().item())},
+        "result": lambda out: _gathered_pairs(out, n, args.n_pairs),
     }
+
+
+def _sha(a) -> str:
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _gathered_pairs(out, n_local: int, n_pairs: int) -> dict:
+    """After the timed region: every rank's scores gathered in global pair order
+    (search.gather_pairs -- the optional config-3 exchange), summarised."""
+    from paper_1909_00899_b200 import search
+
+    allsc = search.gather_pairs(out["score"][:n_local], n_pairs).cpu().numpy()
+    return {"score_sum": int(allsc.astype(np.int64).sum()), "scores_sha256": _sha(allsc)}
 
 
 # ---- configs 1, 4, 5 (single pair) ----------------------------------------------------
@@ -881,6 +897,7 @@ def main() -> None:
     e2e_ms = timer.max_over_ranks(e2e_ms)
     e2e_value = cells / (e2e_ms / args.steps * 1e-3) / 1e9
 
+    result = d["result"](last)  # collective for config 3: every rank takes part
     if rank == 0:
         hbm = hbm_peak()
         hbm_achieved = d["alg_bytes"] / (k_ms * 1e-3) / 1e9
@@ -908,7 +925,7 @@ def main() -> None:
                     "d2h_bytes_per_step": int(d["d2h"])},
             "gpu_launches": int(gpu_launches),
             "clocks": clocks,
-            **d["result"](last),
+            **result,
         }
         if variants:
             line["variants"] = variants

@@ -72,6 +72,28 @@ def shard_pairs(n_pairs: int, rank: int, world: int) -> tuple[int, int]:
     return a, b
 
 
+def gather_pairs(local: torch.Tensor, n_pairs: int, group=None) -> torch.Tensor:
+    """Per-pair results of contiguous pair shards (shard_pairs) gathered on every
+    rank in global pair order: one all_gather of each rank's [b - a, ...] block,
+    padded to the largest shard (NCCL on device tensors, gloo on host tensors).
+    The only exchange config 3 has, and an optional one."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return local[:n_pairs]
+    world = dist.get_world_size(group)
+    dev = local.device
+    if dist.get_backend(group) == "gloo":
+        local = local.cpu()
+    sizes = [b - a for a, b in (shard_pairs(n_pairs, r, world) for r in range(world))]
+    mx = max(sizes)
+    pad = torch.zeros((mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    return torch.cat([p[:n] for p, n in zip(parts, sizes)]).to(dev)
+
+
 PACKED_FILES = ("codes", "start", "length", "order", "ids")
 
 

@@ -53,7 +53,16 @@ def _body(rank, world, out_q):
         local = search.topk_records(torch.from_numpy(sc), packed.ids, torch.from_numpy(re_),
                                     torch.from_numpy(qe), 25)
         merged = search.merge_topk(local, 25)
-        out_q.put((rank, ids, int(packed.residues), merged.numpy()))
+        # config 3: each rank generates only its own pair range and aligns it; the
+        # optional result gather restores global pair order on every rank
+        n3 = 3000
+        a, b = search.shard_pairs(n3, rank, world)
+        w3 = W.config3(n_pairs=n3, start=a, stop=b)
+        s3, r3, q3 = O.batch_scalar(w3.flat_q, w3.q_off, w3.flat_r, w3.r_off,
+                                    sub=w3.scheme.as_array(), go=6, ge=1)
+        local3 = torch.from_numpy(np.stack([s3, r3, q3], axis=1).astype(np.int32))
+        gathered = search.gather_pairs(local3, n3)
+        out_q.put((rank, ids, int(packed.residues), merged.numpy(), gathered.numpy()))
 
 
 def test_shard_and_topk_merge_world2():
@@ -83,5 +92,11 @@ def test_shard_and_topk_merge_world2():
                                torch.from_numpy(re_), torch.from_numpy(qe), 25).numpy()
     for r in res:
         assert (r[3] == want).all()
+    w3 = W.config3(n_pairs=3000)
+    s3, r3, q3 = O.batch_scalar(w3.flat_q, w3.q_off, w3.flat_r, w3.r_off,
+                                sub=w3.scheme.as_array(), go=6, ge=1)
+    want3 = np.stack([s3, r3, q3], axis=1).astype(np.int32)
+    for r in res:
+        assert (r[4] == want3).all(), "gathered config-3 shards == single-process batch"
     # order: score desc, then id asc among ties
     assert all((a[0] > b[0]) or (a[0] == b[0] and a[1] < b[1]) for a, b in zip(want, want[1:]))
