@@ -27,6 +27,9 @@ namespace swb {
 #ifndef SWB_CHAIN_SLEEP
 #define SWB_CHAIN_SLEEP 1
 #endif
+#ifndef SWB_CHAIN_RADIX
+#define SWB_CHAIN_RADIX 1  // 32-bit strips: radix-8 scan on F shifted by two lanes
+#endif
 #ifndef SWB_CHAIN_BP_ALL
 // Back-pressure spin by every lane.  With only the writing lane spinning (divergent),
 // the head strip's warp stayed in a degraded issue mode afterwards: ~9x slower columns
@@ -256,10 +259,15 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
       const int fin = tin.x;
       const int hlk = tin.y;
       // diagonal for the strip's first cell: corrected H of strip b-1, column i-1
-      uint32_t vh = Wd::template shift<T, 1>(wnext, t, gmask, sel[0]);
-      if (t == 0) {  // lane 0 (low half of thread 0) takes the previous strip's value
-        constexpr uint32_t keep = Wd::LPW == 2 ? 0xffff0000u : 0u;
-        vh = (vh & keep) | (Wd::pack(hd_prev, 0) & ~keep);
+      uint32_t vh;
+      if constexpr (Wd::LPW == 1 && SWB_CHAIN_RADIX) {
+        vh = wnext;  // already the lane-shifted wrap (lane 0: strip b-1's value)
+      } else {
+        vh = Wd::template shift<T, 1>(wnext, t, gmask, sel[0]);
+        if (t == 0) {  // lane 0 (low half of thread 0) takes the previous strip's value
+          constexpr uint32_t keep = Wd::LPW == 2 ? 0xffff0000u : 0u;
+          vh = (vh & keep) | (Wd::pack(hd_prev, 0) & ~keep);
+        }
       }
       hd_prev = hlk;
       uint32_t F = 0u;
@@ -313,6 +321,46 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
         int g = max(gb, cmx);
         g = __reduce_max_sync(gmask, g);  // one REDUX for the strip-wide best
         gb = g;
+      }
+      if constexpr (Wd::LPW == 1 && SWB_CHAIN_RADIX) {
+        // 32-bit strips: Alg. 6's scan as a radix-8 weighted max-plus prefix (two
+        // rounds of independent shuffles instead of five dependent ones), run on F
+        // shifted by TWO lanes so it yields G[l] = carry[l-1] directly:
+        //   carry[l] = max(F[l-1], G[l] - L*ge)            (the lane's carry)
+        //   wrap[l]  = max(H[l-1][L-1], G[l] - (L-1)*ge)   (next column's word-0 diagonal)
+        // -- the wrap no longer waits for a shuffle of the finished carry.
+        // Lanes below a shuffle distance receive their own value, which the max-plus
+        // step leaves unchanged (every value is >= 0).
+        const int d = min(L * ge, cl);
+        const int f = (int)F;
+        int f1 = __shfl_up_sync(gmask, f, 1);
+        int f2 = __shfl_up_sync(gmask, f, 2);
+        int hs = __shfl_up_sync(gmask, (int)H[L - 1], 1);
+        f1 = t == 0 ? fin : f1;               // lane 0: the F entering the strip
+        f2 = t == 1 ? fin : (t == 0 ? 0 : f2);
+        hs = t == 0 ? hlk : hs;               // lane 0: strip b-1's corrected last H
+        int y1 = __shfl_up_sync(gmask, f2, 1), y2 = __shfl_up_sync(gmask, f2, 2),
+            y3 = __shfl_up_sync(gmask, f2, 3), y4 = __shfl_up_sync(gmask, f2, 4),
+            y5 = __shfl_up_sync(gmask, f2, 5), y6 = __shfl_up_sync(gmask, f2, 6),
+            y7 = __shfl_up_sync(gmask, f2, 7);
+        const int q1 = __viaddmax_s32(y1, -d, f2), q2 = __viaddmax_s32(y3, -d, y2);
+        const int q3 = __viaddmax_s32(y5, -d, y4), q4 = __viaddmax_s32(y7, -d, y6);
+        const int r1 = __viaddmax_s32(q2, -2 * d, q1), r2 = __viaddmax_s32(q4, -2 * d, q3);
+        const int w8 = __viaddmax_s32(r2, -4 * d, r1);  // window of 8 lanes
+        const int z1 = __shfl_up_sync(gmask, w8, 8), z2 = __shfl_up_sync(gmask, w8, 16),
+                  z3 = __shfl_up_sync(gmask, w8, 24);
+        const int p1 = __viaddmax_s32(z1, -8 * d, w8), p2 = __viaddmax_s32(z3, -8 * d, z2);
+        const int g = __viaddmax_s32(p2, -16 * d, p1);  // carry[l-1]
+        carry = (uint32_t)__viaddmax_s32(g, -d, f1);
+        wnext = (uint32_t)__viaddmax_s32(g, -(int)min((int64_t)(L - 1) * ge, (int64_t)cl), hs);
+        const uint32_t fo = Wd::addmax(carry, NLD, F);  // true F leaving each lane
+        if (t == T - 1) {
+          // the boundary H of this column: lane 31's corrected last word
+          const int hlast = __viaddmax_s32((int)carry, -(int)min((int64_t)(L - 1) * ge,
+                                                                 (int64_t)cl), (int)H[L - 1]);
+          tile_out[col_k] = make_int2((int)fo, hlast);
+        }
+        continue;
       }
       // Alg. 6 scan inside the strip, then fold in the strip's incoming F
       uint32_t acc = Wd::template shift_in<T>(F, Wd::splat(fin), t, gmask, sel_in);
