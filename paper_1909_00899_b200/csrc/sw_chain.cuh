@@ -251,11 +251,24 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
     tile_in[t] = make_int4(fin_l, hl_l, t < kc ? (int)__ldg(a.ref + t0 + t) : 0, 0);
     __syncwarp();
 
+    // profile words of the tile's first column; each column then loads the next
+    // column's words before its own work, so the two dependent shared-memory loads
+    // (residue, then profile row) leave the column's critical path
+    uint32_t Sc[L];
+    {
+      const uint32_t* pr0 = prof_t + tile_in[0].z * (L * 32);
+#pragma unroll
+      for (int c = 0; c < L; ++c) Sc[c] = pr0[c * 32];
+    }
     for (int col_k = 0; col_k < kc; ++col_k) {
       const int64_t i = t0 + col_k;
       const int4 tin = tile_in[col_k];
-      const int sym = tin.z;
-      const uint32_t* pr = prof_t + sym * (L * 32);
+      uint32_t Sn[L];
+      {
+        const uint32_t* pr1 = prof_t + tile_in[min(col_k + 1, kc - 1)].z * (L * 32);
+#pragma unroll
+        for (int c = 0; c < L; ++c) Sn[c] = pr1[c * 32];
+      }
       const int fin = tin.x;
       const int hlk = tin.y;
       // diagonal for the strip's first cell: corrected H of strip b-1, column i-1
@@ -277,7 +290,7 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
       for (int ch = 0; ch < kNch; ++ch) cmk[ch] = 0u;
 #pragma unroll
       for (int c = 0; c < L; ++c) {
-        const uint32_t S = pr[c * 32];
+        const uint32_t S = Sc[c];
         const uint32_t u = Wd::addmax(vh, S, E[c]);
         const uint32_t Hn = Wd::vmax(u, F);
         const uint32_t Xu = Wd::add(u, NGO);
@@ -360,6 +373,8 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
                                                                  (int64_t)cl), (int)H[L - 1]);
           tile_out[col_k] = make_int2((int)fo, hlast);
         }
+#pragma unroll
+        for (int c = 0; c < L; ++c) Sc[c] = Sn[c];
         continue;
       }
       // Alg. 6 scan inside the strip, then fold in the strip's incoming F
@@ -381,6 +396,8 @@ __global__ void __launch_bounds__(32) sw_chain_kernel(const ChainArgs a) {
       // the strip's last lane (thread 31, top half) holds this column's boundary
       // pair; stage it so the tile leaves in one coalesced store
       if (t == T - 1) tile_out[col_k] = make_int2(Wd::get(fo, Wd::LPW - 1), Wd::get(wnext, Wd::LPW - 1));
+#pragma unroll
+      for (int c = 0; c < L; ++c) Sc[c] = Sn[c];
     }
     __syncwarp();
     if (b + 1 < nb && t < kc) {

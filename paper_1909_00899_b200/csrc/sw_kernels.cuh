@@ -260,6 +260,12 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #ifndef SWB_COL_UNROLL
 #define SWB_COL_UNROLL 1  // reference columns per loop iteration (unroll factor)
 #endif
+#ifndef SWB_COL_UNROLL_SHORT
+#define SWB_COL_UNROLL_SHORT 1  // the same for exact instances of <= SWB_SHORT_L words
+#endif
+#ifndef SWB_SHORT_L
+#define SWB_SHORT_L 24
+#endif
 #define SWB_PRAGMA(x) _Pragma(#x)
 #define SWB_UNROLL(n) SWB_PRAGMA(unroll n)
 
@@ -285,6 +291,7 @@ sw_striped_kernel(const SwArgs a) {
   // never conflicts (DB mode: two copies; pairs mode: two groups interleaved).
   constexpr bool DUP = VEC && T == 4;
   constexpr int BW = DUP ? 32 : T * 4;  // words per (sym, j4) block
+  constexpr int kColUnroll = (EXACT && LMAX <= SWB_SHORT_L) ? SWB_COL_UNROLL_SHORT : SWB_COL_UNROLL;
 
   extern __shared__ uint32_t smem[];
 
@@ -524,7 +531,7 @@ sw_striped_kernel(const SwArgs a) {
     const int nullsym = A;
     int nxt = (len > 0) ? (int)__ldcg(tp) : nullsym;
 
-    SWB_UNROLL(SWB_COL_UNROLL)
+#pragma unroll kColUnroll
     for (int i = 0; i < maxlen; ++i) {
       const int sym = nxt;
       nxt = (i + 1 < len) ? (int)__ldcg(tp + i + 1) : nullsym;
@@ -585,71 +592,75 @@ sw_striped_kernel(const SwArgs a) {
       // the alignment's best grows a few dozen times, not per lane-column).
       // A cell attaining the best is a diagonal cell, so its stored H equals
       // u; the first word with H >= cm is the first such cell in the lane.
-      uint32_t cm = cmk[0];
+      // score-only launches (no coordinate outputs: a launch-uniform branch) skip the
+      // gate entirely -- the chunk maxima already hold the score
+      if (!no_coords) {
+        uint32_t cm = cmk[0];
 #pragma unroll
-      for (int k = 1; k < kNch; ++k) cm = Wd::vmax(cm, cmk[k]);
-      const int cmx = Wd::hmax(cm);
-      if (SNAP && cmx > gb) {
-        bool now = false;
+        for (int k = 1; k < kNch; ++k) cm = Wd::vmax(cm, cmk[k]);
+        const int cmx = Wd::hmax(cm);
+        if (SNAP && cmx > gb) {
+          bool now = false;
 #pragma unroll
-        for (int h = 0; h < Wd::LPW; ++h) {
-          const int cv = Wd::get(cm, h);
-          if (cv > gb && cv > bv) { bv = cv; bcol = i; bh = h; now = true; }
-        }
-        if (now) {
-          // one STS.32 per word at immediate offsets (odd row stride: few bank
-          // conflicts); a 128-bit store would need H in aligned register quads,
-          // which costs ~45 moves per column
+          for (int h = 0; h < Wd::LPW; ++h) {
+            const int cv = Wd::get(cm, h);
+            if (cv > gb && cv > bv) { bv = cv; bcol = i; bh = h; now = true; }
+          }
+          if (now) {
+            // one STS.32 per word at immediate offsets (odd row stride: few bank
+            // conflicts); a 128-bit store would need H in aligned register quads,
+            // which costs ~45 moves per column
 #pragma unroll
-          for (int c = 0; c < LMAX; ++c) snap[c] = H[c];
-        }
-      } else if (!SNAP && cmx > gb) {
+            for (int c = 0; c < LMAX; ++c) snap[c] = H[c];
+          }
+        } else if (!SNAP && cmx > gb) {
 #pragma unroll
-        for (int h = 0; h < Wd::LPW; ++h) {
-          const int cv = Wd::get(cm, h);
-          if (cv > gb && cv > bv) {
-            // the first chunk reaching cv holds the first cell reaching it
-            int kk = 0;
+          for (int h = 0; h < Wd::LPW; ++h) {
+            const int cv = Wd::get(cm, h);
+            if (cv > gb && cv > bv) {
+              // the first chunk reaching cv holds the first cell reaching it
+              int kk = 0;
 #pragma unroll
-            for (int k = kNch - 1; k >= 0; --k)
-              if (Wd::get(cmk[k], h) >= cv) kk = k;
-            int jj;
-            if constexpr (EXACT) {
-              // gather the chunk's words without branching on kk, then search them
-              int jo = kCh;
+              for (int k = kNch - 1; k >= 0; --k)
+                if (Wd::get(cmk[k], h) >= cv) kk = k;
+              int jj;
+              if constexpr (EXACT) {
+                // gather the chunk's words without branching on kk, then search them
+                int jo = kCh;
 #pragma unroll
-              for (int j = kCh - 1; j >= 0; --j) {
-                uint32_t w = 0u;
+                for (int j = kCh - 1; j >= 0; --j) {
+                  uint32_t w = 0u;
 #pragma unroll
-                for (int k = 0; k < kNch; ++k)
-                  if (k * kCh + j < LMAX) w = (k == kk) ? H[k * kCh + j] : w;
-                if (Wd::get(w, h) >= cv) jo = j;  // unused / padding words hold 0 < cv
-              }
-              jj = kk * kCh + jo;
-            } else {
-              jj = first;
+                  for (int k = 0; k < kNch; ++k)
+                    if (k * kCh + j < LMAX) w = (k == kk) ? H[k * kCh + j] : w;
+                  if (Wd::get(w, h) >= cv) jo = j;  // unused / padding words hold 0 < cv
+                }
+                jj = kk * kCh + jo;
+              } else {
+                jj = first;
 #pragma unroll
-              for (int k = 0; k < kNch; ++k) {
-                if (k == kk) {
+                for (int k = 0; k < kNch; ++k) {
+                  if (k == kk) {
 #pragma unroll
-                  for (int c = (k + 1) * kCh - 1; c >= k * kCh; --c)
-                    if (c < LMAX && c >= first && Wd::get(H[c], h) >= cv) jj = c;
+                    for (int c = (k + 1) * kCh - 1; c >= k * kCh; --c)
+                      if (c < LMAX && c >= first && Wd::get(H[c], h) >= cv) jj = c;
+                  }
                 }
               }
+              bv = cv;
+              bcol = i;
+              bq = (h * T + t) * L + (jj - first);
             }
-            bv = cv;
-            bcol = i;
-            bq = (h * T + t) * L + (jj - first);
           }
         }
-      }
-      if (floor_mode) {
-        gb = max(gb, cmx);
-      } else {
-        int g = max(gb, cmx);
+        if (floor_mode) {
+          gb = max(gb, cmx);
+        } else {
+          int g = max(gb, cmx);
 #pragma unroll
-        for (int off = T / 2; off >= 1; off >>= 1) g = max(g, __shfl_xor_sync(cmask, g, off, T));
-        gb = g;
+          for (int off = T / 2; off >= 1; off >>= 1) g = max(g, __shfl_xor_sync(cmask, g, off, T));
+          gb = g;
+        }
       }
 
       // ---- cross-lane F dependency ----

@@ -1,0 +1,19 @@
+"""Profile driver: one 32-bit strip-pipeline launch on a config-5 slice
+(query 16,384 x reference 65,536; SWB_CHAIN_L picks the strip height)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_1909_00899_b200 import align, workloads as W
+
+w = W.config5()
+q, r = w.query[:16384].copy(), w.ref[:65536].copy()
+align.align_long(q, r, w.scheme, width=32)  # warm-up (the profiled launch is the 2nd)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+res = align.align_long(q, r, w.scheme, width=32)
+e1.record()
+torch.cuda.synchronize()
+print(res, f"{e0.elapsed_time(e1):.2f} ms")
