@@ -495,8 +495,10 @@ class Timer:
 
     def __init__(self, stream, world, backend, flush: bool):
         import torch
+        import torch.distributed as dist
 
         self.torch, self.stream, self.world, self.backend = torch, stream, world, backend
+        self.distributed = dist.is_available() and dist.is_initialized()
         self.flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if flush else None
 
     def run(self, fn, steps: int) -> float:
@@ -516,7 +518,7 @@ class Timer:
         return self.max_over_ranks(ms)
 
     def max_over_ranks(self, ms: float) -> float:
-        if self.world > 1:
+        if self.distributed:
             import torch.distributed as dist
 
             t = self.torch.tensor([ms], device="cuda" if self.backend == "nccl" else "cpu")
@@ -830,14 +832,18 @@ def main() -> None:
     backend = os.environ.get("SWB_DIST_BACKEND", "nccl")
     ndev = torch.cuda.device_count()
     torch.cuda.set_device(local % ndev)
-    if world > 1:
+    # under torch.distributed.run the process group is created even for one rank, so
+    # the NCCL path (communicator, barrier, the max-over-ranks reduce and the top-k
+    # all_gather) runs on the device at every N
+    distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
+    if distributed:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local % ndev))
         else:
             dist.init_process_group(backend)
 
     def barrier():
-        if world > 1:
+        if distributed:
             dist.barrier()
 
     L = _lib.load()
@@ -932,7 +938,7 @@ def main() -> None:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(cfg, w, args.cpu_seconds)
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 

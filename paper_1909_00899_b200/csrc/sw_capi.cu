@@ -551,8 +551,13 @@ static ChainGeo chain_geo(int64_t m, int64_t n, int n_sym, int width) {
   double best = 1e300;
   // measured per-column latency (cycles, 32-bit, B200) of one strip alone and of a
   // strip in a full pipeline (~3.5 strips per SM); tools/chain_latency.py
-  static const double lat_alone[6] = {315, 323, 356, 404, 486, 670};
-  static const double lat_loaded[6] = {380, 366, 386, 431, 511, 700};
+  static const double lat_alone16[6] = {315, 323, 356, 404, 486, 670};
+  static const double lat_loaded16[6] = {380, 366, 386, 431, 511, 700};
+  // 32-bit carry-split strips (sw_chain32.cuh), profiles/r02j_chain_latency.txt
+  static const double lat_alone32[6] = {215, 209, 211, 277, 386, 670};
+  static const double lat_loaded32[6] = {240, 232, 240, 312, 448, 700};
+  const double* lat_alone = width == 32 ? lat_alone32 : lat_alone16;
+  const double* lat_loaded = width == 32 ? lat_loaded32 : lat_loaded16;
   for (int li = 0; li < 6; ++li) {
     const int L = Ls[li];
     const int64_t rows = 32LL * lpw * L;
@@ -561,7 +566,8 @@ static ChainGeo chain_geo(int64_t m, int64_t n, int n_sym, int width) {
     const double lat = lat_alone[li] + load * (lat_loaded[li] - lat_alone[li]);
     // every strip must be co-resident (cooperative launch): keep well inside
     // 148 SMs x 16 one-warp CTAs unless no strip height fits
-    double cost = (double)(n + nb * 2 * kChainK) * lat;  // a strip trails by ~2 tiles
+    // a strip trails by ~2 tiles (32-bit: ~3, it starts two tiles behind, sw_chain32.cuh)
+    double cost = (double)(n + nb * (width == 32 ? 3 : 2) * kChainK) * lat;
     if (nb > 148 * 16 && li < 5) cost *= 1e6;
     if (cost < best) {
       best = cost;
@@ -713,7 +719,8 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
   }
   const void* fn = wave ? g_wave[g.li][g.ki] : g_chain[wi][g.li];
   const size_t smem = wave ? (size_t)(n_sym + 1) * g.L * 32 * 4 + 128 * g.KC + 3 * kChainK * g.KC * 8  // residues, tile_in, 2 x tile_out
-                           : (size_t)(n_sym + 1) * g.L * 32 * 4 + (kChainK + 1) * 16 + kChainK * 8;  // + tile staging
+                           : (size_t)(n_sym + 1) * g.L * 32 * 4 + (kChainK + 1) * 16 + kChainK * 8
+                                 + (width == 32 ? (size_t)(n_sym + 1) * 32 * 8 : 0);  // + tile staging, (B, C) table
   if (smem > 48 * 1024) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(chain smem)");

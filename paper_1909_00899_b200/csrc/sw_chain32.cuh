@@ -28,6 +28,9 @@
 #pragma once
 #include "sw_chain.cuh"
 
+#ifndef SWB_CHAIN32_BF_L
+#define SWB_CHAIN32_BF_L 8
+#endif
 #ifndef SWB_CHAIN32_UNROLL
 #define SWB_CHAIN32_UNROLL 2  // columns per loop iteration (register rotation without moves)
 #endif
@@ -38,6 +41,9 @@ template <int L>
 __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
   constexpr int T = 32;
   constexpr int RING = kChainRing * kChainK;
+  // strips of up to SWB_CHAIN32_BF_L words per lane track the first maximum without a
+  // branch (L compares + 4 selects per column instead of a REDUX and a branch)
+  constexpr bool kBranchFree = L <= SWB_CHAIN32_BF_L;
   const int t = threadIdx.x;
   const int b = a.reverse ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;
   const int nb = a.nb;
@@ -55,6 +61,8 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
   // per-tile staging: (F_in, H_last, residue) per column + the next tile's first residue
   int4* tile_in = reinterpret_cast<int4*>(smem + (A_ + 1) * L * 32);
   int2* tile_out = reinterpret_cast<int2*>(tile_in + kChainK + 1);
+  // per (residue, lane): (B, C) of the F_L formula -- they depend on the profile row only
+  int2* bc_tab = reinterpret_cast<int2*>(tile_out + kChainK);
 
   const int CL = W32::CLAMP;
   const int go = min(a.go, CL), ge = min(a.ge, CL);
@@ -67,6 +75,14 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
   for (int c = 0; c < L; ++c) kA[c] = (int)min((int64_t)go + (int64_t)(L - 1 - c) * ge, (int64_t)CL);
   const int nullsym = A_;
   const int keep1 = t >= 1 ? -1 : 0, keep2 = t >= 2 ? -1 : 0;
+  for (int sym = 0; sym <= A_; ++sym) {
+    const int* row = prof_t + sym * (L * 32);
+    int sm = -(1 << 29);
+#pragma unroll
+    for (int c = 1; c < L; ++c) sm = max(sm, row[c * 32]);
+    bc_tab[sym * 32 + t] = make_int2(L >= 2 ? sm - kB : -(1 << 29), row[0] - kC);
+  }
+  __syncwarp();
 
   int H[L], E[L];
 #pragma unroll
@@ -77,17 +93,12 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
   const int64_t n = a.n;
   const int64_t qbase = (int64_t)b * T * L;
 
-  // A, B, C of the next column from its profile row and the current stored state
-  auto abc = [&](const int (&S)[L], int hs, int& Ao, int& Bo, int& Co) {
+  // A of the next column from its profile row and the current stored state
+  auto a_of = [&](const int (&S)[L], int hs) -> int {
     int acc = __viaddmax_s32(hs, S[0], E[0]) - kA[0];
 #pragma unroll
     for (int c = 1; c < L; ++c) acc = max(acc, __viaddmax_s32(H[c - 1], S[c], E[c]) - kA[c]);
-    Ao = acc;
-    int sm = -(1 << 29);
-#pragma unroll
-    for (int c = 1; c < L; ++c) sm = max(sm, S[c]);
-    Bo = L >= 2 ? sm - kB : -(1 << 29);
-    Co = S[0] - kC;
+    return acc;
   };
 
   int2* ring_in = a.ring + (size_t)(b > 0 ? b - 1 : 0) * RING;
@@ -105,10 +116,28 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
   int Sc[L];
   int Acur, Bcur, Ccur;
   {
-    const int* pr0 = prof_t + (int)__ldg(a.ref) * (L * 32);
+    const int sym0 = (int)__ldg(a.ref);
+    const int* pr0 = prof_t + sym0 * (L * 32);
 #pragma unroll
     for (int c = 0; c < L; ++c) Sc[c] = pr0[c * 32];
-    abc(Sc, 0, Acur, Bcur, Ccur);
+    Acur = a_of(Sc, 0);
+    const int2 bc = bc_tab[sym0 * 32 + t];
+    Bcur = bc.x;
+    Ccur = bc.y;
+  }
+  // residues two tiles ahead: res1 = the next tile's, res2 = the one after (clamped
+  // loads, masked when staged, so no instruction waits on a load issued this tile)
+  auto ld_res = [&](int64_t c) -> int { return (int)__ldg(a.ref + min(c, n - 1)); };
+  int res1 = ld_res(t), res2 = ld_res(kChainK + t);
+  // Start two tiles behind strip b-1: the boundary tile prefetched at the start of a
+  // tile is then already written when it is loaded (one tile behind, every prefetch
+  // found the entries stale and the validation paid a full L2 round trip per tile).
+  if (b > 0 && n > kChainK) {
+    const int64_t c1 = kChainK + t;
+    const unsigned want = tag_of(kChainK);
+    while (!__all_sync(gmask, c1 >= n || (unsigned)((ld_relaxed(ring_in64 + (c1 % RING)) >> 31) &
+                                                    1u) == want))
+      __nanosleep(64);
   }
 
   for (int64_t t0 = 0; t0 < n; t0 += kChainK) {
@@ -141,9 +170,14 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
       }
     }
     __syncwarp();
-    tile_in[t] = make_int4(fin_l, hl_l, t < kc ? (int)__ldg(a.ref + t0 + t) : nullsym, 0);
-    if (t == 0)  // the residue after this tile: the last column prepares its A, B, C
-      tile_in[kChainK] = make_int4(0, 0, t0 + kc < n ? (int)__ldg(a.ref + t0 + kc) : nullsym, 0);
+    const int res_here = res1;
+    res1 = res2;
+    res2 = ld_res(t0 + 2 * kChainK + t);
+    tile_in[t] = make_int4(fin_l, hl_l, t < kc ? res_here : nullsym, 0);
+    // the residue after this tile (the next tile's first): the last column prepares
+    // the next column's A, B, C from it
+    const int first_next = __shfl_sync(gmask, res1, 0);
+    if (t == 0) tile_in[kChainK] = make_int4(0, 0, t0 + kc < n ? first_next : nullsym, 0);
     __syncwarp();
 
     int2 fh = *reinterpret_cast<const int2*>(&tile_in[0]);  // (F_in, H_last) of column t0
@@ -161,6 +195,7 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
 #pragma unroll
         for (int c = 0; c < L; ++c) Sn[c] = pr1[c * 32];
       }
+      const int2 bcn = bc_tab[tn.z * 32 + t];
 
       // ---- critical path: F leaving each lane, the radix-8 scan, the carry ----
       const int FL = __viaddmax_s32_relu(G, Ccur, __viaddmax_s32(K, Bcur, Acur));
@@ -204,13 +239,29 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
       int cm = cmk[0];
 #pragma unroll
       for (int k = 1; k < kNch; ++k) cm = max(cm, cmk[k]);
-      const int gb_prev = gb;
-      gb = __reduce_max_sync(gmask, max(gb, cm));  // the strip's best of all columns so far
+      int gb_prev = gb;
+      if constexpr (kBranchFree) {
+        // each lane keeps its own first maximum without a branch: the first column
+        // where its maximum grows, and in it the first word reaching the new value
+        // (a cell reaching the best is a diagonal cell, stored H == u); the strip
+        // and pipeline reductions pick (score desc, column asc, row asc) at the end
+        int jj = L - 1;
+#pragma unroll
+        for (int c = L - 2; c >= 0; --c) jj = H[c] >= cm ? c : jj;
+        const bool up = cm > bv;
+        bv = up ? cm : bv;
+        bcol = up ? (int)i : bcol;
+        bq = up ? (int)(qbase + t * L) + jj : bq;
+      } else {
+        gb = __reduce_max_sync(gmask, max(gb, cm));  // the strip's best of all columns so far
+      }
 
       // ---- next column's A, B, C from this column's stored state ----
       int hsn = __shfl_up_sync(gmask, H[L - 1], 1);
       hsn = t == 0 ? hlk : hsn;  // lane 0: strip b-1's corrected last H of this column
-      abc(Sn, hsn, Acur, Bcur, Ccur);
+      Acur = a_of(Sn, hsn);
+      Bcur = bcn.x;
+      Ccur = bcn.y;
       if (t == T - 1) {
         const int fo = __viaddmax_s32(Kn, -d, F);          // true F leaving the strip
         const int hlast = __viaddmax_s32(Kn, -dw, H[L - 1]);  // its corrected last H
@@ -224,7 +275,7 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
       // end coordinates (rare: the strip's best improved in this lane) -- the only
       // branch of the column, placed after everything the next column needs so the
       // scheduler can interleave the scan with the recurrence above
-      if (SWB_CHAIN_COORDS && cm > gb_prev && cm > bv) {
+      if (!kBranchFree && SWB_CHAIN_COORDS && cm > gb_prev && cm > bv) {
         int kk = 0;
 #pragma unroll
         for (int k = kNch - 1; k >= 0; --k)

@@ -79,7 +79,7 @@ def gather_pairs(local: torch.Tensor, n_pairs: int, group=None) -> torch.Tensor:
     The only exchange config 3 has, and an optional one."""
     import torch.distributed as dist
 
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+    if not (dist.is_available() and dist.is_initialized()):
         return local[:n_pairs]
     world = dist.get_world_size(group)
     dev = local.device
@@ -459,7 +459,7 @@ def merge_topk(records: torch.Tensor, k: int, group=None) -> torch.Tensor:
     """Cross-rank top-k: all_gather k records per rank (NCCL), re-select on every rank."""
     import torch.distributed as dist
 
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+    if not (dist.is_available() and dist.is_initialized()):
         return records
     world = dist.get_world_size(group)
     dev = records.device
