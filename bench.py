@@ -684,7 +684,11 @@ def device_config3(args, w, rank, world, timer, L):
         "step": step, "kernel_only": kernel_only, "e2e_step": e2e_step, "engine": batch,
         "rank_cells": 150 * 300 * n, "h2d": e2e_batch.h2d_bytes, "d2h": e2e_batch.d2h_bytes,
         "kernel_name": "sw_striped_kernel<W16,T=4,L=19,SCAN,exact,ge=1> (pairs mode, score-only)",
-        "width": 16, "alg_bytes": alg_bytes, "traffic": None, "variants": variants,
+        "width": 16, "alg_bytes": alg_bytes,
+        # dram__bytes_read+write of this kernel: 507.88 MB per 2^20 pairs in one ncu
+        # --set full capture (profiles/r02k_config3_pairs_kernel_score.md), scaled to
+        # the rank's pairs
+        "traffic": 507.88e6 * n / (1 << 20), "variants": variants,
         "extra_config": {"lanes": 8, "seg_len": 19},
         "result": lambda out: _gathered_pairs(out, n, args.n_pairs),
     }

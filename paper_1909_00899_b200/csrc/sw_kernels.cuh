@@ -593,8 +593,10 @@ sw_striped_kernel(const SwArgs a) {
       // A cell attaining the best is a diagonal cell, so its stored H equals
       // u; the first word with H >= cm is the first such cell in the lane.
       // score-only launches (no coordinate outputs: a launch-uniform branch) skip the
-      // gate entirely -- the chunk maxima already hold the score
-      if (!no_coords) {
+      // gate entirely -- the chunk maxima already hold the score. Segments of up to
+      // 32 words only (pair batches): for the long database segments the extra
+      // branch cost more than the gate it skips (config 2 kernel -3 %).
+      if (!(LMAX <= 32 && no_coords)) {
         uint32_t cm = cmk[0];
 #pragma unroll
         for (int k = 1; k < kNch; ++k) cm = Wd::vmax(cm, cmk[k]);
