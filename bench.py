@@ -730,15 +730,16 @@ def device_single(cfg, args, w, rank, world, timer, L):
     o3 = (C.c_void_p(out.data_ptr()), C.c_void_p(out.data_ptr() + 4),
           C.c_void_p(out.data_ptr() + 8))
 
-    def long_fn(kernel, width):
+    def long_fn(kernel, width, coords=True):
         nbytes = int(L.sw_long_workspace_bytes(m, n, sch.n_symbols, width))
         ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
         kid = _lib.KERNEL_IDS[kernel]
+        outs = o3 if coords else (o3[0], None, None)
 
         def fn():
             _lib.check(L.sw_align_long(width, kid, _ptr(q), m, _ptr(r), n, _ptr(sub),
                                        sch.n_symbols, sch.gap_open, sch.gap_extend, sch.bias,
-                                       sch.max_score, _ptr(ws), nbytes, *o3, _ptr(fl), _stream()))
+                                       sch.max_score, _ptr(ws), nbytes, *outs, _ptr(fl), _stream()))
         return fn
 
     def warp_fn(kernel, lanes):
@@ -776,18 +777,22 @@ def device_single(cfg, args, w, rank, world, timer, L):
         kname = main_desc + " scan"
     elif cfg == 4:
         launches = 2  # sw_align_long: strip-profile kernel + cooperative strip kernel
-        main_fn, main_desc = long_fn("scan", 32), "scan strip pipeline W32 (sw_align_long)"
-        variants_spec = [("scan-block-p128", *block_fn("scan", 128, 32)),
+        main_fn = long_fn("scan", 32, coords=False)
+        main_desc = "scan strip pipeline W32, score-only (sw_align_long)"
+        variants_spec = [("scan+coords", long_fn("scan", 32), "scan strip pipeline W32 with end coordinates"),
+                         ("scan-block-p128", *block_fn("scan", 128, 32)),
                          ("lazyf-block-p128", *block_fn("lazyf", 128, 32)),
                          ("wavefront", long_fn("wavefront", 32), "wavefront strips W32")]
-        e2e_call = lambda: align.align_long(w.query, w.ref, sch, width=32)  # noqa: E731
-        kname = "sw_chain_kernel<W32> (scan strips)"
+        e2e_call = lambda: align.align_long(w.query, w.ref, sch, width=32, coords=False)  # noqa: E731
+        kname = "sw_chain32_kernel<L, score-only> (carry-split scan strips)"
     else:
         launches = 2
-        main_fn, main_desc = long_fn("scan", 32), "scan strip pipeline W32 (sw_align_long)"
-        variants_spec = [("wavefront", long_fn("wavefront", 32), "wavefront strips W32")]
-        e2e_call = lambda: align.align_long(w.query, w.ref, sch, width=32)  # noqa: E731
-        kname = "sw_chain_kernel<W32> (scan strips)"
+        main_fn = long_fn("scan", 32, coords=False)
+        main_desc = "scan strip pipeline W32, score-only (sw_align_long)"
+        variants_spec = [("scan+coords", long_fn("scan", 32), "scan strip pipeline W32 with end coordinates"),
+                         ("wavefront", long_fn("wavefront", 32), "wavefront strips W32")]
+        e2e_call = lambda: align.align_long(w.query, w.ref, sch, width=32, coords=False)  # noqa: E731
+        kname = "sw_chain32_kernel<L, score-only> (carry-split scan strips)"
 
     def step():
         main_fn()
@@ -813,8 +818,9 @@ def device_single(cfg, args, w, rank, world, timer, L):
         "rank_cells": m * n, "h2d": m + n + sch.n_symbols ** 2, "d2h": 16,
         "kernel_name": kname, "width": 32 if cfg in (4, 5) else 16, "alg_bytes": m + n,
         "traffic": None, "variants": variants, "extra_config": {"path": main_desc},
-        "result": lambda o: {"score": int(o[0].item()), "ref_end": int(o[1].item()),
-                             "query_end": int(o[2].item())},
+        "result": (lambda o: {"score": int(o[0].item()), "ref_end": int(o[1].item()),
+                              "query_end": int(o[2].item())}) if cfg == 1 else
+                  (lambda o: {"score": int(o[0].item())}),  # score-only main launch
         "latency": {"columns": n}, "launches_per_step": launches,
     }
 

@@ -251,10 +251,11 @@ def build_profile_arrays(query, scheme: ScoringScheme, p: int = 0) -> DeviceProf
 
 
 def align_long(query, ref, scheme: ScoringScheme, width: int = 32, kernel: str = "scan",
-               query_dev: torch.Tensor | None = None, ref_dev: torch.Tensor | None = None) -> dict:
+               query_dev: torch.Tensor | None = None, ref_dev: torch.Tensor | None = None,
+               coords: bool = True) -> dict:
     """One long pair through the strip pipeline (sw_align_long). Returns host ints
     ``score, ref_end, query_end, flags``; a 16-bit run that hits the wrap guard is
-    repeated in 32 bits."""
+    repeated in 32 bits. ``coords=False``: score-only launch (ends stay -1)."""
     _require_cuda()
     L = _lib.load()
     qd = query_dev if query_dev is not None else torch.from_numpy(
@@ -275,12 +276,16 @@ def align_long(query, ref, scheme: ScoringScheme, width: int = 32, kernel: str =
         _lib.check(L.sw_align_long(w, _kernel_id(kernel), _ptr(qd), m, _ptr(rd), n, _ptr(sub),
                                    scheme.n_symbols, scheme.gap_open, scheme.gap_extend,
                                    scheme.bias, scheme.max_score, _ptr(ws), int(nbytes),
-                                   C.c_void_p(out.data_ptr()), C.c_void_p(out.data_ptr() + 4),
-                                   C.c_void_p(out.data_ptr() + 8), _ptr(fl), _stream()))
+                                   C.c_void_p(out.data_ptr()),
+                                   C.c_void_p(out.data_ptr() + 4) if coords else None,
+                                   C.c_void_p(out.data_ptr() + 8) if coords else None,
+                                   _ptr(fl), _stream()))
         flags = int(fl.item())
         if not flags & _lib.FLAG_RESCUE:
             break
     o = out.cpu().tolist()
+    if not coords:
+        o[1] = o[2] = -1
     if width == 16 and w == 32:
         flags |= _lib.FLAG_RESCUED
     return {"score": o[0], "ref_end": o[1], "query_end": o[2], "flags": flags & ~_lib.FLAG_RESCUE}
@@ -331,6 +336,8 @@ def align_block(query, ref, scheme: ScoringScheme, p: int = 0, kernel: str = "sc
         if not flags & _lib.FLAG_RESCUE:
             break
     o = out.cpu().tolist()
+    if not coords:
+        o[1] = o[2] = -1
     if width == 16 and w == 32:
         flags |= _lib.FLAG_RESCUED
     res.update(score=o[0], ref_end=o[1], query_end=o[2], flags=flags & ~_lib.FLAG_RESCUE)

@@ -18,6 +18,10 @@
 
 using namespace swb;
 
+#ifndef SWB_CHAIN_SPLIT_SO
+#define SWB_CHAIN_SPLIT_SO 1
+#endif
+
 namespace {
 
 thread_local char g_err[512] = "";
@@ -37,6 +41,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 KernelTable g_tab[2][3];
 ExactTable g_exact;  // 16-bit scan, exact segment length
 const void* g_chain[2][6];  // strip pipeline [width][L = 1, 2, 4, 8, 16, 32]
+const void* g_chain_so[6];  // 32-bit score-only strips [L]
 const void* g_chain_prof[2];
 const void* g_wave[4][4];  // [L = 1, 2, 4, 8][KC = 1, 2, 4, 8]
 const void* g_block[2][3][16];  // block / cluster scan [width][variant][L-1]  // strip pipeline, intra-strip wavefront [L = 1, 2, 4, 8]
@@ -59,7 +64,9 @@ void init_tables() {
   swb_fill_exact_t4_g0_d(g_exact); swb_fill_exact_t4_g1_d(g_exact); swb_fill_exact_t4_g2_d(g_exact);
   swb_fill_exact_t4_g0_e(g_exact); swb_fill_exact_t4_g1_e(g_exact); swb_fill_exact_t4_g2_e(g_exact);
   swb_fill_exact_t4_g0_f(g_exact); swb_fill_exact_t4_g1_f(g_exact); swb_fill_exact_t4_g2_f(g_exact);
-  swb_fill_chain(g_chain, g_chain_prof);
+  // T = 2 (4 stripes): 33..40 words, pair batches of ~150-residue reads at lanes = 4
+  swb_fill_exact_t2_g0_c(g_exact); swb_fill_exact_t2_g1_c(g_exact); swb_fill_exact_t2_g2_c(g_exact);
+  swb_fill_chain(g_chain, g_chain_prof, g_chain_so);
   swb_fill_wave(g_wave);
   swb_fill_block16(g_block[0]);
   swb_fill_block32(g_block[1]);
@@ -428,7 +435,7 @@ int32_t sw_db_align(const sw_plan_t* p, const uint32_t* d_prof, int32_t kernel, 
   // exact instances stage the profile as [sym][ceil(L/4)][T][4]
   // (T = 4: two copies at 32-word block granularity, see DUP in sw_kernels.cuh)
   const size_t prof_bytes = block != 256 ? (size_t)(p->n_sym + 1) * ((p->seg_len + 3) / 4 * 4) * p->threads *
-                                               4 * (p->threads == 4 ? 2 : 1)
+                                               4 * (p->threads <= 4 ? 8 / p->threads : 1)
                                          : (size_t)p->prof_words * 4;
   // + the end-coordinate snapshots (SWB_SNAP): LMAX words per thread, only when
   // coordinates are requested (score-only launches keep their occupancy)
@@ -717,7 +724,11 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
     a.trace_tiles = atoi(getenv("SWB_CHAIN_TRACE_TILES"));
     a.reverse = getenv("SWB_CHAIN_REVERSE") != nullptr;
   }
-  const void* fn = wave ? g_wave[g.li][g.ki] : g_chain[wi][g.li];
+  // score-only launches (no coordinate outputs) of the 32-bit strips skip the
+  // end-coordinate tracking
+  const bool score_only = !d_ref_end && !d_query_end;
+  const void* fn = wave ? g_wave[g.li][g.ki]
+                        : (wi == 1 && score_only && SWB_CHAIN_SPLIT_SO ? g_chain_so[g.li] : g_chain[wi][g.li]);
   const size_t smem = wave ? (size_t)(n_sym + 1) * g.L * 32 * 4 + 128 * g.KC + 3 * kChainK * g.KC * 8  // residues, tile_in, 2 x tile_out
                            : (size_t)(n_sym + 1) * g.L * 32 * 4 + (kChainK + 1) * 16 + kChainK * 8
                                  + (width == 32 ? (size_t)(n_sym + 1) * 32 * 8 : 0);  // + tile staging, (B, C) table

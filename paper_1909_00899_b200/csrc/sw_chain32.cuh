@@ -37,7 +37,7 @@
 
 namespace swb {
 
-template <int L>
+template <int L, bool COORDS = true>
 __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
   constexpr int T = 32;
   constexpr int RING = kChainRing * kChainK;
@@ -240,7 +240,9 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
 #pragma unroll
       for (int k = 1; k < kNch; ++k) cm = max(cm, cmk[k]);
       int gb_prev = gb;
-      if constexpr (kBranchFree) {
+      if constexpr (!COORDS) {
+        bv = max(bv, cm);  // score-only launch: the running maximum is all it needs
+      } else if constexpr (kBranchFree) {
         // each lane keeps its own first maximum without a branch: the first column
         // where its maximum grows, and in it the first word reaching the new value
         // (a cell reaching the best is a diagonal cell, stored H == u); the strip
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
       // end coordinates (rare: the strip's best improved in this lane) -- the only
       // branch of the column, placed after everything the next column needs so the
       // scheduler can interleave the scan with the recurrence above
-      if (!kBranchFree && SWB_CHAIN_COORDS && cm > gb_prev && cm > bv) {
+      if (COORDS && !kBranchFree && SWB_CHAIN_COORDS && cm > gb_prev && cm > bv) {
         int kk = 0;
 #pragma unroll
         for (int k = kNch - 1; k >= 0; --k)

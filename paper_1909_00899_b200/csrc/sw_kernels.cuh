@@ -289,7 +289,9 @@ sw_striped_kernel(const SwArgs a) {
   // of a quarter-warp LDS.128 phase read different symbols: blocks are placed at
   // 32-word granularity with the group parity selecting the half, so the phase
   // never conflicts (DB mode: two copies; pairs mode: two groups interleaved).
-  constexpr bool DUP = VEC && T == 4;
+  // T = 2 likewise with GRP = 4 quarters (four groups per quarter-warp phase).
+  constexpr int GRP = (VEC && T <= 4) ? 32 / (4 * T) : 1;
+  constexpr bool DUP = GRP > 1;
   constexpr int BW = DUP ? 32 : T * 4;  // words per (sym, j4) block
   constexpr int kColUnroll = (EXACT && LMAX <= SWB_SHORT_L) ? SWB_COL_UNROLL_SHORT : SWB_COL_UNROLL;
 
@@ -365,14 +367,15 @@ sw_striped_kernel(const SwArgs a) {
     }
     __syncthreads();
     set_gaps(a.go, a.ge, L);
-    prof_base = VEC ? smem + 4 * t + (DUP ? 16 * (gw & 1) : 0) : smem + t - first * T;
+    prof_base = VEC ? smem + 4 * t + (DUP ? 4 * T * (gw & (GRP - 1)) : 0) : smem + t - first * T;
   } else {
     LT = 0;
     prof_base = nullptr;
   }
   // pairs mode: each group owns a slice of (A+1)*LMAX*T words
   uint32_t* gslice =
-      DUP ? smem + (size_t)((threadIdx.x >> 5) * G + (gw & ~1)) * (size_t)a.pair_stride + 16 * (gw & 1)
+      DUP ? smem + (size_t)((threadIdx.x >> 5) * G + (gw & ~(GRP - 1))) * (size_t)a.pair_stride +
+                4 * T * (gw & (GRP - 1))
           : smem + (size_t)((threadIdx.x >> 5) * G + gw) * (size_t)a.pair_stride;
 
   // Coordinate floor (database top-k): end coordinates are located only for
@@ -919,8 +922,9 @@ SWB_X_DECL(4, 0, e) SWB_X_DECL(4, 1, e) SWB_X_DECL(4, 2, e)
 SWB_X_DECL(4, 0, f) SWB_X_DECL(4, 1, f) SWB_X_DECL(4, 2, f)
 SWB_X_DECL(16, 0, c) SWB_X_DECL(16, 1, c) SWB_X_DECL(16, 2, c)
 SWB_X_DECL(32, 0, c) SWB_X_DECL(32, 1, c) SWB_X_DECL(32, 2, c)
+SWB_X_DECL(2, 0, c) SWB_X_DECL(2, 1, c) SWB_X_DECL(2, 2, c)
 #undef SWB_X_DECL
-void swb_fill_chain(const void* (&tab)[2][6], const void* (&ptab)[2]);
+void swb_fill_chain(const void* (&tab)[2][6], const void* (&ptab)[2], const void* (&so)[6]);
 void swb_fill_wave(const void* (&tab)[4][4]);
 void swb_fill_block16(const void* (&tab)[3][16]);
 void swb_fill_block32(const void* (&tab)[3][16]);

@@ -122,6 +122,9 @@ def test_config5_full_pair_vs_oracle(A, G, kernel):
     r = A.align_long(w.query, w.ref, w.scheme, width=32, kernel=kernel)
     assert (r["score"], r["ref_end"], r["query_end"]) == (want["score"], want["ref_end"],
                                                           want["query_end"])
+    if kernel == "scan":  # the metric's score-only launch (no coordinate tracking)
+        so = A.align_long(w.query, w.ref, w.scheme, width=32, coords=False)
+        assert so["score"] == want["score"] and (so["ref_end"], so["query_end"]) == (-1, -1)
     g = golden("configs.npz")
     if "c5_scan_p64_score" in g.files:  # the reference's own scan kernel agrees
         assert want["score"] == int(g["c5_scan_p64_score"])

@@ -20,14 +20,17 @@ def A():
     return align
 
 
+@pytest.mark.parametrize("lanes", [0, 4])
 @pytest.mark.parametrize("coords", [False, True])
-def test_pairs_batch_resident_and_streamed(A, oracle, coords):
+def test_pairs_batch_resident_and_streamed(A, oracle, coords, lanes):
+    """lanes=0: the throughput layout (8 stripes, 19 words); lanes=4: 4 stripes of 38
+    words (T = 2, four groups interleaved per 32-word profile block)."""
     from paper_1909_00899_b200 import workloads as W
 
     w = W.config3(n_pairs=50_000)
     s, re_, qe = oracle.batch_scalar(w.flat_q, w.q_off, w.flat_r, w.r_off,
                                      sub=w.scheme.as_array(), go=6, ge=1)
-    b = A.PairsBatch(w.scheme, coords=coords)
+    b = A.PairsBatch(w.scheme, coords=coords, lanes=lanes)
     b.upload(w.flat_q, w.q_off, w.flat_r, w.r_off)
     o = b.run()
     assert (o["score"][: w.n_pairs].cpu().numpy() == s).all()
@@ -35,7 +38,7 @@ def test_pairs_batch_resident_and_streamed(A, oracle, coords):
         assert (o["ref_end"][: w.n_pairs].cpu().numpy() == re_).all()
         assert (o["query_end"][: w.n_pairs].cpu().numpy() == qe).all()
     host = A.PairsBatch.pin_host(w.flat_q, w.q_off, w.flat_r, w.r_off)
-    e = A.PairsBatch(w.scheme, coords=coords)
+    e = A.PairsBatch(w.scheme, coords=coords, lanes=lanes)
     e.prepare_host(host, n_chunks=7)
     for _ in range(2):  # buffers are reused across calls
         h = e.run_host(host)
@@ -77,3 +80,23 @@ def test_pairs_batch_mixed_lengths_and_rescue(A, oracle):
     h = e.run_host(host)
     torch.cuda.synchronize()
     assert (h["score"].numpy() == s).all() and (h["query_end"].numpy() == qe).all()
+
+
+def test_database_search_four_stripes(A, oracle):
+    """The T = 2 exact instances in database mode (four profile copies interleaved per
+    32-word block): a 150-residue query at lanes=4, every target against the oracle."""
+    from paper_1909_00899_b200 import search, workloads as W
+
+    w = W.config2(n_targets=3000)
+    q = w.query[:150].copy()
+    packed = search.pack(w.db, w.offsets, pin=False)
+    eng = search.DatabaseSearch(w.scheme, coords="all", lanes=4)
+    eng.upload(packed)
+    eng.set_query(q)
+    assert (eng.plan16.lanes, eng.plan16.seg_len) == (4, 38)
+    o = eng.align()
+    ids = packed.ids.numpy()
+    s, re_, qe = oracle.db_scalar(q, w.db, w.offsets, w.scheme.as_array(), 11, 1)
+    assert (o["score"][: w.n_targets].cpu().numpy() == s[ids]).all()
+    assert (o["ref_end"][: w.n_targets].cpu().numpy() == re_[ids]).all()
+    assert (o["query_end"][: w.n_targets].cpu().numpy() == qe[ids]).all()

@@ -530,6 +530,35 @@ def test_long_pair_pipeline_random(A, oracle):
         assert (got["score"], got["ref_end"], got["query_end"]) == want, (trial, "wave", m, n)
 
 
+@pytest.mark.parametrize("rows_per_lane", [1, 2, 4, 8, 16, 32])
+def test_chain32_strip_heights(A, oracle, rows_per_lane, monkeypatch):
+    """The 32-bit carry-split strips (sw_chain32.cuh) at every strip height, with end
+    coordinates (branch-free first maximum up to 8 rows per lane, gated above) and
+    score-only, on random schemes and ragged sizes, against the oracle."""
+    from paper_1909_00899_b200.scoring import ScoringScheme
+
+    monkeypatch.setenv("SWB_CHAIN_L", str(rows_per_lane))
+    rng = np.random.default_rng(0xC32 + rows_per_lane)
+    for trial in range(6):
+        k = int(rng.integers(2, 21))
+        mat = rng.integers(-5, 6, (k, k))
+        go = int(rng.integers(1, 12))
+        ge = int(rng.integers(1, go + 1))
+        sch = ScoringScheme.from_array(mat, go, ge)
+        m = int(rng.integers(1, 6000))
+        n = int(rng.integers(1, 2500))
+        q = rng.integers(0, k, m).astype(np.uint8)
+        r = rng.integers(0, k, n).astype(np.uint8)
+        if trial % 2:
+            blk = q[: min(m, n)]
+            r[: blk.shape[0]] = blk
+        want = oracle.scalar(q, r, mat, go, ge)
+        got = A.align_long(q, r, sch, width=32)
+        assert (got["score"], got["ref_end"], got["query_end"]) == want, (trial, m, n)
+        so = A.align_long(q, r, sch, width=32, coords=False)
+        assert so["score"] == want[0], (trial, m, n)
+
+
 @pytest.mark.parametrize("cols_per_step", [1, 2, 4, 8])
 @pytest.mark.parametrize("rows_per_lane", [1, 2, 4, 8])
 def test_wavefront_strip_heights(A, oracle, rows_per_lane, cols_per_step, monkeypatch):

@@ -9,7 +9,8 @@ import torch
 from paper_1909_00899_b200 import align, workloads as W
 
 w = W.config3(n_pairs=1 << 20)
-b = align.PairsBatch(w.scheme, coords=os.environ.get("C3_COORDS") == "1")
+b = align.PairsBatch(w.scheme, coords=os.environ.get("C3_COORDS") == "1",
+                     lanes=int(os.environ.get("C3_LANES", "0")))
 b.upload(w.flat_q, w.q_off, w.flat_r, w.r_off)
 b.run()
 torch.cuda.synchronize()
