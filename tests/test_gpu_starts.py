@@ -104,13 +104,12 @@ def test_runner_starts_columns(A, oracle):
     lines = [x for x in buf.getvalue().splitlines() if not x.startswith("#")]
     assert lines[0].endswith("ref_end\tquery_end\tref_start\tquery_start")
     alpha, sch = runner._build_scheme(cfg)
-    named = runner._load_pairs(cfg, alpha)
-    lut = alpha.lut()
+    ps = runner.load_pairs(cfg, alpha)
     sub = sch.as_array()
-    for row, (_, _, qs, ts) in zip(lines[1:], named):
+    for i, row in enumerate(lines[1:]):
         f = row.split("\t")
-        q = lut[np.frombuffer(qs.encode(), np.uint8)]
-        t = lut[np.frombuffer(ts.encode(), np.uint8)]
+        q = ps.fq[ps.q_off[i]:ps.q_off[i + 1]]
+        t = ps.fr[ps.r_off[i]:ps.r_off[i + 1]]
         score, rend, qend = oracle.scalar(q, t, sub, 5, 2)
         assert (int(f[4]), int(f[9]), int(f[10])) == (score, rend, qend)
         assert (int(f[11]), int(f[12])) == oracle.start_coords(q, t, sub, 5, 2, score, rend, qend)

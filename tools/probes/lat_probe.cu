@@ -26,6 +26,12 @@ __global__ void chain(int iters, int a, int b, int* out, long long* cyc) {
       if (V == 8) x = __vimax_s32_relu(x, a);           // VIMNMX.RELU
       if (V == 9) x = (x > a) ? x : b;                  // ISETP+SEL
     }
+    if (V == 10) {  // throughput: 32 independent shuffles per iteration, one warp
+      int acc = 0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) acc += __shfl_up_sync(~0u, x + k, (k & 7) + 1);
+      x = acc;
+    }
   }
   long long t1 = clock64();
   if (threadIdx.x == 0) cyc[0] = t1 - t0;
@@ -38,9 +44,10 @@ int main() {
   cudaMalloc(&out, 4096);
   cudaMallocManaged(&cyc, 64);
   const char* names[] = {"VIADDMNMX", "VIADDMNMX.RELU", "IMNMX(max)", "VIMNMX3", "IADD",
-                         "IMAD", "LDS", "SHFL", "VIMNMX.RELU", "ISETP+SEL"};
+                         "IMAD", "LDS", "SHFL", "VIMNMX.RELU", "ISETP+SEL",
+                         "SHFL indep. (per shfl)"};
   const int iters = 2000;
-  for (int v = 0; v < 10; ++v) {
+  for (int v = 0; v < 11; ++v) {
     for (int rep = 0; rep < 2; ++rep) {
       switch (v) {
         case 0: chain<0><<<1, 32>>>(iters, 3, -1, out, cyc); break;
@@ -52,7 +59,8 @@ int main() {
         case 6: chain<6><<<1, 32>>>(iters, 3, -1, out, cyc); break;
         case 7: chain<7><<<1, 32>>>(iters, 3, -1, out, cyc); break;
         case 8: chain<8><<<1, 32>>>(iters, 3, -1, out, cyc); break;
-        default: chain<9><<<1, 32>>>(iters, 3, -1, out, cyc); break;
+        case 9: chain<9><<<1, 32>>>(iters, 3, -1, out, cyc); break;
+        default: chain<10><<<1, 32>>>(iters, 3, -1, out, cyc); break;
       }
       cudaDeviceSynchronize();
     }
