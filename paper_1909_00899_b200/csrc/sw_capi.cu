@@ -731,7 +731,7 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
                         : (wi == 1 && score_only && SWB_CHAIN_SPLIT_SO ? g_chain_so[g.li] : g_chain[wi][g.li]);
   const size_t smem = wave ? (size_t)(n_sym + 1) * g.L * 32 * 4 + 128 * g.KC + 3 * kChainK * g.KC * 8  // residues, tile_in, 2 x tile_out
                            : (size_t)(n_sym + 1) * g.L * 32 * 4 + (kChainK + 1) * 16 + kChainK * 8
-                                 + (width == 32 ? (size_t)(n_sym + 1) * 32 * 8 : 0);  // + tile staging, (B, C) table
+                                 + (width == 32 ? (size_t)(n_sym + 1) * 32 * 8 + 1024 : 0);  // + tile staging, (B, C) table, scan buffers
   if (smem > 48 * 1024) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(chain smem)");

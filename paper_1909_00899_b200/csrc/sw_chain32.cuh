@@ -28,6 +28,9 @@
 #pragma once
 #include "sw_chain.cuh"
 
+#ifndef SWB_CHAIN32_SMEM_SCAN
+#define SWB_CHAIN32_SMEM_SCAN 0  // 1: the radix-8 scan through shared memory instead of shuffles
+#endif
 #ifndef SWB_CHAIN32_BF_L
 #define SWB_CHAIN32_BF_L 8
 #endif
@@ -63,6 +66,10 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
   int2* tile_out = reinterpret_cast<int2*>(tile_in + kChainK + 1);
   // per (residue, lane): (B, C) of the F_L formula -- they depend on the profile row only
   int2* bc_tab = reinterpret_cast<int2*>(tile_out + kChainK);
+  // shared-memory scan buffers (SWB_CHAIN32_SMEM_SCAN): [column parity][round][64],
+  // the lower 32 entries of every buffer stay zero
+  int* sbuf = reinterpret_cast<int*>(bc_tab + (A_ + 1) * 32);
+  for (int k = t; k < 256; k += 32) sbuf[k] = 0;
 
   const int CL = W32::CLAMP;
   const int go = min(a.go, CL), ge = min(a.ge, CL);
@@ -199,6 +206,28 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
 
       // ---- critical path: F leaving each lane, the radix-8 scan, the carry ----
       const int FL = __viaddmax_s32_relu(G, Ccur, __viaddmax_s32(K, Bcur, Acur));
+#if SWB_CHAIN32_SMEM_SCAN
+      // the same radix-8 scan through shared memory: one store of F (and of the F
+      // entering the strip, at slot 31), a warp barrier, and each lane reads its eight
+      // predecessors of the shifted-by-two vector directly (zeros below lane 0), so no
+      // shift instruction precedes the window; buffers alternate with the column
+      int* b1 = sbuf + (col_k & 1) * 128;
+      int* b2 = b1 + 64;
+      b1[32 + t] = FL;
+      if (t == 0) b1[31] = fin;
+      __syncwarp();
+      const int* rw = b1 + 30 + t;  // rw[-k] = F shifted by two, lane t - k
+      const int f2 = rw[0], y1 = rw[-1], y2 = rw[-2], y3 = rw[-3], y4 = rw[-4], y5 = rw[-5],
+                y6 = rw[-6], y7 = rw[-7];
+      const int f1 = b1[31 + t];
+      const int q1 = __viaddmax_s32(y1, -d, f2), q2 = __viaddmax_s32(y3, -d, y2);
+      const int q3 = __viaddmax_s32(y5, -d, y4), q4 = __viaddmax_s32(y7, -d, y6);
+      const int w8 = __viaddmax_s32(__viaddmax_s32(q4, -2 * d, q3), -4 * d,
+                                    __viaddmax_s32(q2, -2 * d, q1));
+      b2[32 + t] = w8;
+      __syncwarp();
+      const int z1 = b2[24 + t], z2 = b2[16 + t], z3 = b2[8 + t];
+#else
       // lane 0 of the shift by one and lane 1 of the shift by two take the F entering
       // the strip, lane 0 of the shift by two nothing: (x & keep) | inject, one LOP3
       const int f1 = (__shfl_up_sync(gmask, FL, 1) & keep1) | (t == 0 ? fin : 0);
@@ -213,6 +242,7 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
                                     __viaddmax_s32(q2, -2 * d, q1));
       const int z1 = __shfl_up_sync(gmask, w8, 8), z2 = __shfl_up_sync(gmask, w8, 16),
                 z3 = __shfl_up_sync(gmask, w8, 24);
+#endif
       const int gn = __viaddmax_s32(__viaddmax_s32(z3, -8 * d, z2), -16 * d,
                                     __viaddmax_s32(z1, -8 * d, w8));  // carry[l-1]
       const int Kn = __viaddmax_s32(gn, -d, f1);                       // carry[l]
