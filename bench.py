@@ -660,7 +660,7 @@ def device_config3(args, w, rank, world, timer, L):
 
     host = batch.pin_host(w.flat_q, w.q_off, w.flat_r, w.r_off)
     e2e_batch = PairsBatch(w.scheme, kernel=args.kernel, coords=False)
-    e2e_batch.prepare_host(host, n_chunks=16)
+    e2e_batch.prepare_host(host, n_chunks=64)  # 64 chunks: the first copy (not overlapped) is 1/64 of the batch
 
     def e2e_step():
         out = e2e_batch.run_host(host)

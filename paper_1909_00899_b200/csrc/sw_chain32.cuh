@@ -35,7 +35,10 @@
 #define SWB_CHAIN32_BF_L 8
 #endif
 #ifndef SWB_CHAIN32_UNROLL
-#define SWB_CHAIN32_UNROLL 2  // columns per loop iteration (register rotation without moves)
+#define SWB_CHAIN32_UNROLL 2  // columns per loop iteration, coordinate instances
+#endif
+#ifndef SWB_CHAIN32_UNROLL_SO
+#define SWB_CHAIN32_UNROLL_SO 4  // score-only instances (config 5: 2 -> 116.7 ms, 4 -> 110.4, 8 -> 128.9)
 #endif
 
 namespace swb {
@@ -47,6 +50,7 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
   // strips of up to SWB_CHAIN32_BF_L words per lane track the first maximum without a
   // branch (L compares + 4 selects per column instead of a REDUX and a branch)
   constexpr bool kBranchFree = L <= SWB_CHAIN32_BF_L;
+  constexpr int kColUnroll = COORDS ? SWB_CHAIN32_UNROLL : SWB_CHAIN32_UNROLL_SO;
   const int t = threadIdx.x;
   const int b = a.reverse ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;
   const int nb = a.nb;
@@ -188,7 +192,7 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
     __syncwarp();
 
     int2 fh = *reinterpret_cast<const int2*>(&tile_in[0]);  // (F_in, H_last) of column t0
-    SWB_UNROLL(SWB_CHAIN32_UNROLL)
+#pragma unroll kColUnroll
     for (int col_k = 0; col_k < kc; ++col_k) {
       const int64_t i = t0 + col_k;
       const int fin = fh.x, hlk = fh.y;
