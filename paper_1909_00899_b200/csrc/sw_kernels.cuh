@@ -76,6 +76,15 @@ __device__ __forceinline__ uint32_t w4(const uint4& v, int k) {
 }
 
 // ---- word policies -------------------------------------------------------
+#ifndef SWB_IMAD_SHIFT
+#define SWB_IMAD_SHIFT 1  // lane shifts: multiply by 1 / 65536 (IMAD, FMA pipe) instead of PRMT (ALU pipe)
+#endif
+__device__ __forceinline__ uint32_t mul_lo(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
 struct W16 {
   static constexpr int LPW = 2;
   static constexpr int NULLV = -16384;   // null-residue row (beyond a target's end)
@@ -106,11 +115,20 @@ struct W16 {
       return v << 16;
     } else {
       uint32_t r = __shfl_sync(gmask, v, (t - K) & (T - 1), T);
+#if SWB_IMAD_SHIFT
+      // the cell update saturates the ALU pipe; r * 65536 == r << 16 runs on the FMA pipe
+      return mul_lo(r, sel);
+#else
       return prmt(r, 0u, sel);
+#endif
     }
   }
   __device__ static __forceinline__ uint32_t shift_sel(int t, int k) {
+#if SWB_IMAD_SHIFT
+    return t >= k ? 1u : 0x10000u;
+#else
     return t >= k ? 0x3210u : 0x1044u;  // r<<16: bytes {0,0,r0,r1}
+#endif
   }
   // scan shift: like shift, but source-less lanes keep their own value (bytes {v0,v1,r0,r1})
   template <int T, int K>
@@ -257,6 +275,24 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #ifndef SWB_OWN_GATE
 #define SWB_OWN_GATE 1
 #endif
+#ifndef SWB_PACKED_GATE
+#define SWB_PACKED_GATE 0  // measured slower (config 2 kernel 28.21 -> 28.53 ms, config 3 with coordinates 190 -> 201 ms)
+#endif
+#ifndef SWB_FUSE3
+#define SWB_FUSE3 1  // 3-input deferred correction (see FUSE3 in the kernel)
+#endif
+#ifndef SWB_PREF_D
+#define SWB_PREF_D 8  // residue prefetch distance in columns (segments of <= 32 words)
+#endif
+#ifndef SWB_PREF_D_LONG
+#define SWB_PREF_D_LONG 1  // the same for longer segments (a column outlasts the load)
+#endif
+#ifndef SWB_FUSE3_UNROLL
+#define SWB_FUSE3_UNROLL 2
+#endif
+#ifndef SWB_FUSE3_MAXL
+#define SWB_FUSE3_MAXL 32  // longest segment using it (3 state words per query word)
+#endif
 #ifndef SWB_COL_UNROLL
 #define SWB_COL_UNROLL 1  // reference columns per loop iteration (unroll factor)
 #endif
@@ -293,7 +329,22 @@ sw_striped_kernel(const SwArgs a) {
   constexpr int GRP = (VEC && T <= 4) ? 32 / (4 * T) : 1;
   constexpr bool DUP = GRP > 1;
   constexpr int BW = DUP ? 32 : T * 4;  // words per (sym, j4) block
-  constexpr int kColUnroll = (EXACT && LMAX <= SWB_SHORT_L) ? SWB_COL_UNROLL_SHORT : SWB_COL_UNROLL;
+
+  // FUSE3 (exact scan instances with a compile-time gap extend): the stored H of a
+  // word, max(u, F), is only ever read by the next column's deferred correction
+  // max(carry - j*ge, H).  Keeping u and the F that entered the word instead turns
+  // those two ALU-pipe maxima into one 3-input maximum,
+  //   vh = max3(carry - j*ge, u_old, F_old)            VIMNMX3  (ALU pipe)
+  //   cj = cj - ge  (carry - j*ge, running down the words)  VIADD (FMA-lite pipe)
+  // i.e. 4.5 ALU-pipe instructions per packed word instead of 5.5 (the ALU pipe is
+  // the bound; the adds issue beside it), at the price of a third state word.
+  constexpr bool FUSE3 = SWB_FUSE3 && VAR == VAR_SCAN && EXACT && GE > 0 && LMAX <= SWB_FUSE3_MAXL;
+  // two columns per iteration let the register allocator rename u / F into the state
+  // words instead of copying them (one IMAD.MOV per word and column otherwise)
+  constexpr int kColUnroll = FUSE3 ? SWB_FUSE3_UNROLL
+                                   : (EXACT && LMAX <= SWB_SHORT_L) ? SWB_COL_UNROLL_SHORT : SWB_COL_UNROLL;
+
+  constexpr int kPref = LMAX <= 32 ? SWB_PREF_D : SWB_PREF_D_LONG;
 
   extern __shared__ uint32_t smem[];
 
@@ -509,6 +560,9 @@ sw_striped_kernel(const SwArgs a) {
     uint32_t H[LMAX], E[LMAX];
 #pragma unroll
     for (int c = 0; c < LMAX; ++c) { H[c] = 0u; E[c] = 0u; }
+    uint32_t Fs[FUSE3 ? LMAX : 1];  // FUSE3: the F entering each word (H[] then holds u)
+#pragma unroll
+    for (int c = 0; c < (FUSE3 ? LMAX : 1); ++c) Fs[c] = 0u;
     uint32_t carry = 0u;
     int64_t tot_passes = 0, breaks = 0;  // lazy-F statistics (reference op counters)
     // best of all earlier columns: group-wide, or (floor mode) own best and floor - 1;
@@ -524,6 +578,10 @@ sw_striped_kernel(const SwArgs a) {
     const bool floor_mode = floor_v > 0 || (SNAP && SWB_OWN_GATE);
     // score-only launches (no coordinate outputs) never search: the gate never opens
     int gb = no_coords ? 0x7fffffff : floor_mode ? floor_v - 1 : 0;
+    // packed copy of the per-thread gate level (each half: floor - 1 and the half's own best)
+    constexpr bool kPackedGate = SWB_PACKED_GATE && SNAP && SWB_OWN_GATE;
+    uint32_t gbp = Wd::splat(min(max(gb, 0), Wd::LPW == 2 ? 32767 : 0x7fffffff));
+    (void)gbp;
     int bv = 0, bcol = -1, bq = -1;   // this thread's first-maximum record
     int bh = 0;                       // SNAP: the half (lane) holding bv
     // running maxima of u per chunk of kCh words (never reset: a chunk reaches a
@@ -532,12 +590,19 @@ sw_striped_kernel(const SwArgs a) {
 #pragma unroll
     for (int k = 0; k < kNch; ++k) cmk[k] = 0u;
     const int nullsym = A;
-    int nxt = (len > 0) ? (int)__ldcg(tp) : nullsym;
+    // residues are fetched kPref columns ahead (a byte queue in registers): with short
+    // segments a column is shorter than an L2 round trip, and the profile row address
+    // (sym * LT) stalled on the load issued one column earlier (long-scoreboard stalls)
+    int nq[kPref];
+#pragma unroll
+    for (int d = 0; d < kPref; ++d) nq[d] = (d < len) ? (int)__ldcg(tp + d) : nullsym;
 
 #pragma unroll kColUnroll
     for (int i = 0; i < maxlen; ++i) {
-      const int sym = nxt;
-      nxt = (i + 1 < len) ? (int)__ldcg(tp + i + 1) : nullsym;
+      const int sym = nq[0];
+#pragma unroll
+      for (int d = 0; d + 1 < kPref; ++d) nq[d] = nq[d + 1];
+      nq[kPref - 1] = (i + kPref < len) ? (int)__ldcg(tp + i + kPref) : nullsym;
       const uint32_t* pr = prof_base + sym * LT;
       uint4 S4[VEC ? LP4 : 1];
       if constexpr (VEC) {
@@ -551,12 +616,28 @@ sw_striped_kernel(const SwArgs a) {
       constexpr bool kConverged = VAR == VAR_SCAN;
       const uint32_t cmask = kConverged ? 0xffffffffu : gmask;
       uint32_t w = H[LMAX - 1];
-      if constexpr (VAR == VAR_SCAN) w = Wd::addmax(carry, NWRAP, w);
+      if constexpr (FUSE3) w = Wd::vmax(Wd::vmax(Wd::add(carry, NWRAP), w), Fs[LMAX - 1]);
+      else if constexpr (VAR == VAR_SCAN) w = Wd::addmax(carry, NWRAP, w);
       uint32_t vh = Wd::template shift<T, 1>(w, t, cmask, sel[0]);
       uint32_t F = 0u;
+      uint32_t cj = carry;  // FUSE3: carry - j*ge for the word being read
+      (void)cj;
 
+      // max(x - ge, y, 0): the E / F decay
+      auto decay_relu = [&](uint32_t x, uint32_t y) -> uint32_t { return Wd::addmax_relu(x, NGE, y); };
 #define SWB_WORD_BODY(C)                                                   \
-  {                                                                        \
+  if constexpr (FUSE3) {                                                   \
+    const uint32_t S = w4(S4[VEC ? (C) / 4 : 0], (C) & 3);                 \
+    const uint32_t u = Wd::addmax(vh, S, E[C]);                            \
+    const uint32_t Xu = Wd::add(u, NGO);                                   \
+    E[C] = decay_relu(E[C], Xu);                                           \
+    vh = Wd::vmax(Wd::vmax(cj, H[C]), Fs[C]);                              \
+    cj = Wd::add(cj, NGE);                                                 \
+    H[C] = u;                                                              \
+    Fs[C] = F;                                                             \
+    F = decay_relu(F, Xu);                                                 \
+    cmk[(C) / kCh] = Wd::vmax(cmk[(C) / kCh], u);                          \
+  } else {                                                                 \
     const uint32_t S = VEC ? w4(S4[VEC ? (C) / 4 : 0], (C) & 3) : pr[(C) * T]; \
     const uint32_t u = Wd::addmax(vh, S, E[C]);                            \
     const uint32_t Hn = Wd::vmax(u, F);                                    \
@@ -564,8 +645,8 @@ sw_striped_kernel(const SwArgs a) {
     if constexpr (VAR == VAR_LAZYF_MIRROR)                                 \
       E[C] = Wd::addmax_relu(E[C], NGE, Wd::add(Hn, NGO));                 \
     else                                                                   \
-      E[C] = Wd::addmax_relu(E[C], NGE, Xu);                               \
-    F = Wd::addmax_relu(F, NGE, Xu);                                       \
+      E[C] = decay_relu(E[C], Xu);                                         \
+    F = decay_relu(F, Xu);                                                 \
     cmk[(C) / kCh] = Wd::vmax(cmk[(C) / kCh], u);                          \
     if constexpr (VAR == VAR_SCAN) vh = Wd::addmax(carry, NJ[C], H[C]);    \
     else vh = H[C];                                                        \
@@ -603,6 +684,16 @@ sw_striped_kernel(const SwArgs a) {
         uint32_t cm = cmk[0];
 #pragma unroll
         for (int k = 1; k < kNch; ++k) cm = Wd::vmax(cm, cmk[k]);
+        // packed gate: the running maxima never decrease, so a column raises a half's
+        // best exactly when max(cm, gbp) != gbp -- one packed max and one compare on
+        // the common path instead of unpack + scalar max + compare + scalar max
+        bool gate_open = true;
+        if constexpr (kPackedGate) {
+          const uint32_t g2 = Wd::vmax(cm, gbp);
+          gate_open = g2 != gbp;
+          gbp = g2;
+        }
+        if (gate_open) {
         const int cmx = Wd::hmax(cm);
         if (SNAP && cmx > gb) {
           bool now = false;
@@ -665,6 +756,7 @@ sw_striped_kernel(const SwArgs a) {
 #pragma unroll
           for (int off = T / 2; off >= 1; off >>= 1) g = max(g, __shfl_xor_sync(cmask, g, off, T));
           gb = g;
+        }
         }
       }
 
