@@ -293,6 +293,15 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #ifndef SWB_FUSE3_MAXL
 #define SWB_FUSE3_MAXL 32  // longest segment using it (3 state words per query word)
 #endif
+#ifndef SWB_FUSE3_PARTIAL
+#define SWB_FUSE3_PARTIAL 30  // longer segments: the first N words use it (register budget)
+#endif
+#ifndef SWB_FUSE3_REGS
+#define SWB_FUSE3_REGS 146  // state-word budget (2 per word + 1 per fused word)
+#endif
+#ifndef SWB_FUSE3_PARTIAL_UNROLL
+#define SWB_FUSE3_PARTIAL_UNROLL 2
+#endif
 #ifndef SWB_COL_UNROLL
 #define SWB_COL_UNROLL 1  // reference columns per loop iteration (unroll factor)
 #endif
@@ -341,7 +350,16 @@ sw_striped_kernel(const SwArgs a) {
   constexpr bool FUSE3 = SWB_FUSE3 && VAR == VAR_SCAN && EXACT && GE > 0 && LMAX <= SWB_FUSE3_MAXL;
   // two columns per iteration let the register allocator rename u / F into the state
   // words instead of copying them (one IMAD.MOV per word and column otherwise)
-  constexpr int kColUnroll = FUSE3 ? SWB_FUSE3_UNROLL
+  // longer segments fuse only their first KF words: a fused word keeps three state
+  // registers (u, entering F, E), so 2*LMAX + KF stays inside the register file
+  // (measured on config 2, L = 58: 24 / 30 / 36 / 42 / 57 fused words -> 27.77 / 27.48 /
+  // 27.57 / 29.20 / 28.87 ms against 28.40 ms unfused)
+  constexpr int kFuseBudget = SWB_FUSE3_REGS - (T >= 16 ? 20 : 0) - 2 * LMAX;
+  constexpr int kFuseWords = kFuseBudget < SWB_FUSE3_PARTIAL ? (kFuseBudget < 0 ? 0 : kFuseBudget) : SWB_FUSE3_PARTIAL;
+  constexpr int KF = FUSE3 ? LMAX
+                     : (SWB_FUSE3 && VAR == VAR_SCAN && EXACT && GE > 0) ? (kFuseWords < LMAX ? kFuseWords : LMAX - 1)
+                                                                         : 0;  // words in the fused form
+  constexpr int kColUnroll = FUSE3 ? SWB_FUSE3_UNROLL : KF > 0 ? SWB_FUSE3_PARTIAL_UNROLL
                                    : (EXACT && LMAX <= SWB_SHORT_L) ? SWB_COL_UNROLL_SHORT : SWB_COL_UNROLL;
 
   constexpr int kPref = LMAX <= 32 ? SWB_PREF_D : SWB_PREF_D_LONG;
@@ -560,9 +578,9 @@ sw_striped_kernel(const SwArgs a) {
     uint32_t H[LMAX], E[LMAX];
 #pragma unroll
     for (int c = 0; c < LMAX; ++c) { H[c] = 0u; E[c] = 0u; }
-    uint32_t Fs[FUSE3 ? LMAX : 1];  // FUSE3: the F entering each word (H[] then holds u)
+    uint32_t Fs[KF > 0 ? KF : 1];  // fused words: the F entering the word (H[] then holds u)
 #pragma unroll
-    for (int c = 0; c < (FUSE3 ? LMAX : 1); ++c) Fs[c] = 0u;
+    for (int c = 0; c < (KF > 0 ? KF : 1); ++c) Fs[c] = 0u;
     uint32_t carry = 0u;
     int64_t tot_passes = 0, breaks = 0;  // lazy-F statistics (reference op counters)
     // best of all earlier columns: group-wide, or (floor mode) own best and floor - 1;
@@ -626,7 +644,7 @@ sw_striped_kernel(const SwArgs a) {
       // max(x - ge, y, 0): the E / F decay
       auto decay_relu = [&](uint32_t x, uint32_t y) -> uint32_t { return Wd::addmax_relu(x, NGE, y); };
 #define SWB_WORD_BODY(C)                                                   \
-  if constexpr (FUSE3) {                                                   \
+  if ((C) < KF) {                                                          \
     const uint32_t S = w4(S4[VEC ? (C) / 4 : 0], (C) & 3);                 \
     const uint32_t u = Wd::addmax(vh, S, E[C]);                            \
     const uint32_t Xu = Wd::add(u, NGO);                                   \
