@@ -281,8 +281,11 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #ifndef SWB_FUSE3
 #define SWB_FUSE3 1  // 3-input deferred correction (see FUSE3 in the kernel)
 #endif
+#ifndef SWB_IMM_DECAY
+#define SWB_IMM_DECAY 1
+#endif
 #ifndef SWB_PREF_D
-#define SWB_PREF_D 8  // residue prefetch distance in columns (segments of <= 32 words)
+#define SWB_PREF_D 0  // residue prefetch distance in columns (segments of <= 32 words); 0: the unroll factor
 #endif
 #ifndef SWB_PREF_D_LONG
 #define SWB_PREF_D_LONG 1  // the same for longer segments (a column outlasts the load)
@@ -362,7 +365,8 @@ sw_striped_kernel(const SwArgs a) {
   constexpr int kColUnroll = FUSE3 ? SWB_FUSE3_UNROLL : KF > 0 ? SWB_FUSE3_PARTIAL_UNROLL
                                    : (EXACT && LMAX <= SWB_SHORT_L) ? SWB_COL_UNROLL_SHORT : SWB_COL_UNROLL;
 
-  constexpr int kPref = LMAX <= 32 ? SWB_PREF_D : SWB_PREF_D_LONG;
+  // a queue as deep as the unroll factor rotates by register renaming (no moves)
+  constexpr int kPref = LMAX <= 32 ? (SWB_PREF_D > 0 ? SWB_PREF_D : kColUnroll) : SWB_PREF_D_LONG;
 
   extern __shared__ uint32_t smem[];
 
@@ -642,7 +646,18 @@ sw_striped_kernel(const SwArgs a) {
       (void)cj;
 
       // max(x - ge, y, 0): the E / F decay
-      auto decay_relu = [&](uint32_t x, uint32_t y) -> uint32_t { return Wd::addmax_relu(x, NGE, y); };
+      // (compile-time ge: a fresh single-use constant per call, so ptxas folds it into the
+      // instruction as an immediate instead of holding it in a register -- a third
+      // register source can collide in the register-file banks)
+      auto decay_relu = [&](uint32_t x, uint32_t y) -> uint32_t {
+        if constexpr (GE > 0 && SWB_IMM_DECAY) {
+          uint32_t k;
+          asm volatile("mov.b32 %0, %1;" : "=r"(k) : "n"(Wd::splat(-GE)));
+          return Wd::addmax_relu(x, k, y);
+        } else {
+          return Wd::addmax_relu(x, NGE, y);
+        }
+      };
 #define SWB_WORD_BODY(C)                                                   \
   if ((C) < KF) {                                                          \
     const uint32_t S = w4(S4[VEC ? (C) / 4 : 0], (C) & 3);                 \
