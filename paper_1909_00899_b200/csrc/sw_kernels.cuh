@@ -290,6 +290,9 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #ifndef SWB_PREF_D_LONG
 #define SWB_PREF_D_LONG 1  // the same for longer segments (a column outlasts the load)
 #endif
+#ifndef SWB_FUSE3_CHAIN
+#define SWB_FUSE3_CHAIN 4  // carry - j*ge: this many interleaved running adds down the words
+#endif
 #ifndef SWB_FUSE3_UNROLL
 #define SWB_FUSE3_UNROLL 2
 #endif
@@ -642,8 +645,14 @@ sw_striped_kernel(const SwArgs a) {
       else if constexpr (VAR == VAR_SCAN) w = Wd::addmax(carry, NWRAP, w);
       uint32_t vh = Wd::template shift<T, 1>(w, t, cmask, sel[0]);
       uint32_t F = 0u;
-      uint32_t cj = carry;  // FUSE3: carry - j*ge for the word being read
-      (void)cj;
+      // fused words: carry - j*ge for the word being read, as kCjS interleaved running
+      // adds (each value feeds a maximum and the next add, which keeps ptxas from folding
+      // the add back into a VIADDMNMX; one chain would put L dependent adds behind the scan)
+      constexpr int kCjS = SWB_FUSE3_CHAIN;
+      const uint32_t NSGE = Wd::splat(-(GE > 0 ? GE : 1) * kCjS);
+      uint32_t cjs[kCjS];
+#pragma unroll
+      for (int k = 0; k < kCjS; ++k) cjs[k] = (k == 0 || KF == 0) ? carry : Wd::add(carry, NJ[k < LMAX ? k : 0]);
 
       // max(x - ge, y, 0): the E / F decay
       // (compile-time ge: a fresh single-use constant per call, so ptxas folds it into the
@@ -664,8 +673,8 @@ sw_striped_kernel(const SwArgs a) {
     const uint32_t u = Wd::addmax(vh, S, E[C]);                            \
     const uint32_t Xu = Wd::add(u, NGO);                                   \
     E[C] = decay_relu(E[C], Xu);                                           \
-    vh = Wd::vmax(Wd::vmax(cj, H[C]), Fs[C]);                              \
-    cj = Wd::add(cj, NGE);                                                 \
+    vh = Wd::vmax(Wd::vmax(cjs[(C) % kCjS], H[C]), Fs[C]);                  \
+    cjs[(C) % kCjS] = Wd::add(cjs[(C) % kCjS], NSGE);                      \
     H[C] = u;                                                              \
     Fs[C] = F;                                                             \
     F = decay_relu(F, Xu);                                                 \
