@@ -369,7 +369,8 @@ sw_striped_kernel(const SwArgs a) {
                                    : (EXACT && LMAX <= SWB_SHORT_L) ? SWB_COL_UNROLL_SHORT : SWB_COL_UNROLL;
 
   // a queue as deep as the unroll factor rotates by register renaming (no moves)
-  constexpr int kPref = LMAX <= 32 ? (SWB_PREF_D > 0 ? SWB_PREF_D : kColUnroll) : SWB_PREF_D_LONG;
+  // (runtime-L instances also serve single pairs, where one warp waits out every load: 4 ahead)
+  constexpr int kPref = LMAX <= 32 ? (SWB_PREF_D > 0 ? SWB_PREF_D : EXACT ? kColUnroll : 4) : SWB_PREF_D_LONG;
 
   extern __shared__ uint32_t smem[];
 
@@ -537,6 +538,10 @@ sw_striped_kernel(const SwArgs a) {
     }
     const int len = (valid && feed_ok) ? __ldcg(a.t_len + job) : 0;
     const uint8_t* tp = a.tgt + ((valid && feed_ok) ? __ldcg(a.t_start + job) : 0);
+    // keep the pointer itself in registers: left to itself ptxas re-adds the base from
+    // the constant bank every column (LDC + 3-input add), and the in-order wait on that
+    // LDC costs a single-warp launch ~50 cycles per column
+    asm volatile("" : "+l"(tp));
 
     if (a.mode == 1) {
       // ---- per-job query profile (pairs mode) ----
