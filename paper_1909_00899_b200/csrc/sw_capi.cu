@@ -536,7 +536,7 @@ int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8
   const size_t per_thread =
       (size_t)(n_sym + 1) * lslice * 4 + (snap ? (size_t)(lmax_k | 1) * 4 : 0);
   while (block > 32 && per_thread * block > 110 * 1024) block >>= 1;
-  const size_t smem = per_thread * block;
+  const size_t smem = per_thread * block + kPairSubWords * 4;  // + the staged matrix
   if (smem > 227 * 1024) return fail(SW_ENOTSUP, "pair profile slice too large (%zu B)", smem);
   const int G = 32 / p.threads;
   const int64_t tasks = d_n_jobs ? 0 : (n + G - 1) / G;

@@ -52,6 +52,7 @@ enum : uint8_t {
 };
 
 constexpr int kMaxSym = 32;  // alphabet size limit of the device path (plus one null row)
+constexpr int kPairSubWords = kMaxSym * kMaxSym / 4;  // pairs mode: the int8 matrix staged in shared memory
 
 __device__ __forceinline__ int ld_acquire_s32(const int32_t* p) {
   int v;
@@ -449,11 +450,19 @@ sw_striped_kernel(const SwArgs a) {
     LT = 0;
     prof_base = nullptr;
   }
-  // pairs mode: each group owns a slice of (A+1)*LMAX*T words
+  // pairs mode: the substitution matrix (int8 [A][A]) in the first kPairSubWords words,
+  // then each group owns a slice of (A+1)*LMAX*T words
+  uint32_t* const pbase = smem + (a.mode == 1 ? kPairSubWords : 0);
+  const int8_t* const subs = reinterpret_cast<const int8_t*>(smem);
+  if (a.mode == 1 && a.sub != nullptr) {
+    int8_t* dst = reinterpret_cast<int8_t*>(smem);
+    for (int w = threadIdx.x; w < A * A; w += blockDim.x) dst[w] = a.sub[w];
+    __syncthreads();
+  }
   uint32_t* gslice =
-      DUP ? smem + (size_t)((threadIdx.x >> 5) * G + (gw & ~(GRP - 1))) * (size_t)a.pair_stride +
+      DUP ? pbase + (size_t)((threadIdx.x >> 5) * G + (gw & ~(GRP - 1))) * (size_t)a.pair_stride +
                 4 * T * (gw & (GRP - 1))
-          : smem + (size_t)((threadIdx.x >> 5) * G + gw) * (size_t)a.pair_stride;
+          : pbase + (size_t)((threadIdx.x >> 5) * G + gw) * (size_t)a.pair_stride;
 
   // Coordinate floor (database top-k): end coordinates are located only for
   // alignments scoring >= *coord_floor, so the per-column gate compares against
@@ -487,7 +496,7 @@ sw_striped_kernel(const SwArgs a) {
   // end-coordinate snapshots: SNW words per thread after the profile / the slices
   const int prof_w = a.mode == 0 ? (VEC ? (A + 1) * LP4 * BW : (A + 1) * L * T)
                                  : (int)(blockDim.x / T) * a.pair_stride;
-  uint32_t* const snap = smem + (prof_w + 3) / 4 * 4 + threadIdx.x * SNW;
+  uint32_t* const snap = pbase + (prof_w + 3) / 4 * 4 + threadIdx.x * SNW;
   (void)snap;
 
   // Task claiming: with a counter, warps take the next task (in length-descending
@@ -560,25 +569,61 @@ sw_striped_kernel(const SwArgs a) {
       set_gaps(go, ge, L);
       const uint8_t* qp = a.qry + (valid ? a.q_start[job] : 0);
       LT = L * T;
-      for (int sym = 0; sym <= A; ++sym) {
-        for (int j = 0; j < L; ++j) {
-          int v[2];
+      if constexpr (VEC) {
+        // Four word positions at a time: the thread's 8 query residues (two halves) are
+        // read once, then every symbol's four words are filled from them with the
+        // matrix in shared memory and stored as one 128-bit word -- the query is not
+        // re-read per symbol and no global load sits inside the symbol loop.
+        for (int j4 = 0; j4 < LP4; ++j4) {
+          uint32_t cl = 0u, ch = 0u;  // 4 residue codes per half, 0xff = pad
 #pragma unroll
-          for (int h = 0; h < Wd::LPW; ++h) {
-            const int q = (h * T + t) * L + j;
-            int s;
-            if (sym == A) s = Wd::NULLV;
-            else if (q >= m) s = -bias;  // reference pad: profile 0 == -bias (src/profile.py:60-63)
-            else {
-              const int qs = qp[q];
-              s = pp ? (qs == sym ? mt : mm) : (int)a.sub[sym * A + qs];
-            }
-            v[h] = s;
+          for (int k = 0; k < 4; ++k) {
+            const int j = 4 * j4 + k;
+            const int q0 = t * L + j, q1 = (T + t) * L + j;
+            const uint32_t c0 = (j < L && q0 < m) ? (uint32_t)qp[q0] : 0xffu;
+            const uint32_t c1 = (Wd::LPW == 2 && j < L && q1 < m) ? (uint32_t)qp[q1] : 0xffu;
+            cl |= c0 << (8 * k);
+            ch |= c1 << (8 * k);
           }
-          if constexpr (VEC)
-            gslice[(sym * LP4 + (j >> 2)) * BW + t * 4 + (j & 3)] = Wd::pack(v[0], v[1]);
-          else
+          for (int sym = 0; sym <= A; ++sym) {
+            const int8_t* srow = subs + (sym < A ? sym : 0) * A;
+            uint32_t wv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              int v[2] = {0, 0};
+#pragma unroll
+              for (int h = 0; h < Wd::LPW; ++h) {
+                const int qs = (int)(((h ? ch : cl) >> (8 * k)) & 0xffu);
+                int sv;
+                if (sym == A) sv = Wd::NULLV;
+                else if (qs == 0xff) sv = -bias;  // reference pad: profile 0 == -bias (src/profile.py:60-63)
+                else sv = pp ? (qs == sym ? mt : mm) : (int)srow[qs & 31];
+                v[h] = sv;
+              }
+              wv[k] = Wd::pack(v[0], v[1]);
+            }
+            *reinterpret_cast<uint4*>(gslice + (sym * LP4 + j4) * BW + t * 4) =
+                make_uint4(wv[0], wv[1], wv[2], wv[3]);
+          }
+        }
+      } else {
+        for (int sym = 0; sym <= A; ++sym) {
+          for (int j = 0; j < L; ++j) {
+            int v[2];
+#pragma unroll
+            for (int h = 0; h < Wd::LPW; ++h) {
+              const int q = (h * T + t) * L + j;
+              int sv;
+              if (sym == A) sv = Wd::NULLV;
+              else if (q >= m) sv = -bias;  // reference pad: profile 0 == -bias (src/profile.py:60-63)
+              else {
+                const int qs = qp[q];
+                sv = pp ? (qs == sym ? mt : mm) : (int)subs[sym * A + qs];
+              }
+              v[h] = sv;
+            }
             gslice[(sym * L + j) * T + t] = Wd::pack(v[0], v[1]);
+          }
         }
       }
       if constexpr (VEC) LT = LP4 * BW;
