@@ -291,6 +291,9 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #ifndef SWB_PREF_D_LONG
 #define SWB_PREF_D_LONG 1  // the same for longer segments (a column outlasts the load)
 #endif
+#ifndef SWB_RADIX_SCAN
+#define SWB_RADIX_SCAN 0  // (measured: config 3 score-only 126.1 -> 128.5 ms, config 2 +0.2 %) T = 4: one round of independent shuffles + a max tree instead of 3 dependent steps
+#endif
 #ifndef SWB_FUSE3_CHAIN
 #define SWB_FUSE3_CHAIN 4  // carry - j*ge: this many interleaved running adds down the words
 #endif
@@ -391,6 +394,12 @@ sw_striped_kernel(const SwArgs a) {
   uint32_t sel[6];
 #pragma unroll
   for (int s = 0; s < 6; ++s) sel[s] = Wd::shift_sel(t, 1 << s);
+
+  // radix scan (T = 4): selectors of the shifts by 3, 5, 6 and 7 lanes (multipliers)
+  const uint32_t rsel3 = t >= 3 ? 1u : 0x10000u;
+  const uint32_t hsel[2] = {t >= 1 ? 0x10000u : 0u, t >= 2 ? 0x10000u : 0u};
+  const uint32_t hsel3 = t >= 3 ? 0x10000u : 0u;
+  (void)rsel3; (void)hsel; (void)hsel3;
 
   // per-job constants
   int L = 0, first = 0, m = 0;
@@ -853,7 +862,27 @@ sw_striped_kernel(const SwArgs a) {
       }
 
       // ---- cross-lane F dependency ----
-      if constexpr (VAR == VAR_SCAN) {
+      if constexpr (VAR == VAR_SCAN && SWB_RADIX_SCAN && T == 4 && Wd::LPW == 2 && SWB_IMAD_SHIFT) {
+        // 8 stripes in 4 threads: the same weighted scan (src/_compiled.py:320-336) as one
+        // round of three independent shuffles of F itself instead of three dependent
+        // shuffle steps: carry[l] = relu(max_{k=1..7} F[l-k] - (k-1) d), the seven shifted
+        // copies (k and k+4 lanes from each shuffle, k = 4 from the word itself) combined
+        // by a depth-3 tree -- three more maxima per column, half the latency from F to
+        // the carry every word of the next column waits for.
+        const uint32_t r1 = __shfl_sync(cmask, F, (t - 1) & 3, 4);
+        const uint32_t r2 = __shfl_sync(cmask, F, (t - 2) & 3, 4);
+        const uint32_t r3 = __shfl_sync(cmask, F, (t - 3) & 3, 4);
+        const uint32_t s1 = mul_lo(r1, sel[0]), s5 = mul_lo(r1, hsel[0]);  // shifts by 1 and 5 lanes
+        const uint32_t s2 = mul_lo(r2, sel[1]), s6 = mul_lo(r2, hsel[1]);  // 2 and 6
+        const uint32_t s3 = mul_lo(r3, rsel3), s7 = mul_lo(r3, hsel3);     // 3 and 7
+        const uint32_t s4 = F << 16;                                        // 4
+        const uint32_t t1 = Wd::addmax(s2, NKD[0], s1);
+        const uint32_t t2 = Wd::addmax(s4, NKD[0], s3);
+        const uint32_t t3 = Wd::addmax(s6, NKD[0], s5);
+        const uint32_t u1 = Wd::addmax(t2, NKD[1], t1);
+        const uint32_t u2 = Wd::addmax(s7, NKD[1], t3);
+        carry = Wd::addmax_relu(u2, NKD[2], u1);
+      } else if constexpr (VAR == VAR_SCAN) {
         uint32_t acc = Wd::template shift<T, 1>(F, t, cmask, sel[0]);
         // Alg. 6 weighted max-scan, k = 1, 2, 4, ... (src/_compiled.py:320-336)
 #define SWB_STEP(S)                                                                         \
