@@ -189,6 +189,20 @@ int32_t sw_align_block(int32_t width, int32_t kernel, int32_t lanes, const uint8
 int32_t sw_collect_flagged(const uint8_t* d_flags, int64_t n, uint8_t mask, int32_t* d_list,
                            int64_t* d_count, sw_stream_t stream);
 
+/* Top-k of a database search on the device (BASELINE.json config 2's top-100 merge;
+ * the reference has no database driver, its runner aligns pairs,
+ * src/runner.py:141-153).  d_records: int64 [k][4] = (score, target id, ref_end,
+ * query_end), score descending, then target id ascending; rows past min(k, n) are
+ * -1.  d_ids (nullable: the index itself) maps an alignment to its global target id
+ * (< 2^32); d_ref_end / d_query_end nullable (-1).  d_work: sw_topk_workspace()
+ * bytes of device scratch.  1 <= k <= 1024.  Three small launches on `stream`
+ * (score histogram + threshold, compaction, one-CTA sort); mass ties beyond the
+ * 4,096 candidates the sort holds take an exact single-CTA radix select. */
+int64_t sw_topk_workspace(void);
+int32_t sw_topk(const int32_t* d_score, const int64_t* d_ids, const int32_t* d_ref_end,
+                const int32_t* d_query_end, int64_t n, int32_t k, int64_t* d_records,
+                void* d_work, sw_stream_t stream);
+
 /* Device weighted max-plus scan over P lanes (reference weighted_max_scan /
  * _weighted_max_scan_c, src/kernels.py:177-201, src/_compiled.py:448-460):
  * d_f, d_out: uint16 [n][lanes]; d_d: decay per vector.  Values must fit the

@@ -33,6 +33,8 @@ EXPORTS = (
     "sw_db_align",
     "sw_pairs_align",
     "sw_collect_flagged",
+    "sw_topk_workspace",
+    "sw_topk",
     "sw_scan_lanes",
     "sw_dpx_probe",
     "sw_long_workspace_bytes",
@@ -127,6 +129,10 @@ def load():
                                  i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.sw_collect_flagged.restype = i32
     L.sw_collect_flagged.argtypes = [vp, i64, C.c_uint8, vp, vp, vp]
+    L.sw_topk_workspace.restype = i64
+    L.sw_topk_workspace.argtypes = []
+    L.sw_topk.restype = i32
+    L.sw_topk.argtypes = [vp, vp, vp, vp, i64, i32, vp, vp, vp]
     L.sw_scan_lanes.restype = i32
     L.sw_scan_lanes.argtypes = [i32, i32, vp, vp, i32, vp, vp]
     L.sw_dpx_probe.restype = i64

@@ -831,6 +831,22 @@ int32_t sw_collect_flagged(const uint8_t* d_flags, int64_t n, uint8_t mask, int3
   return e == cudaSuccess ? SW_OK : cuda_fail(e, "sw_collect_kernel");
 }
 
+int32_t swb_topk_launch(const int32_t* d_score, const int64_t* d_ids, const int32_t* d_ref_end,
+                        const int32_t* d_query_end, int64_t n, int32_t k, int64_t* d_records,
+                        void* d_work, sw_stream_t stream, const char** err);
+
+int32_t sw_topk(const int32_t* d_score, const int64_t* d_ids, const int32_t* d_ref_end,
+                const int32_t* d_query_end, int64_t n, int32_t k, int64_t* d_records,
+                void* d_work, sw_stream_t stream) {
+  if (!d_score || !d_records || !d_work) return fail(SW_EINVAL, "NULL argument");
+  if (n < 0) return fail(SW_EINVAL, "n < 0");
+  if (k < 1 || k > 1024) return fail(SW_ENOTSUP, "top-k supports 1 <= k <= 1024, got %d", k);
+  const char* what = "";
+  const int32_t rc = swb_topk_launch(d_score, d_ids, d_ref_end, d_query_end, n, k, d_records,
+                                     d_work, stream, &what);
+  return rc == 0 ? SW_OK : cuda_fail((cudaError_t)rc, what);
+}
+
 int32_t sw_scan_lanes(int32_t width, int32_t lanes, const uint16_t* d_f, const int32_t* d_d,
                       int32_t n, uint16_t* d_out, sw_stream_t stream) {
   if (!d_f || !d_d || !d_out) return fail(SW_EINVAL, "NULL argument");

@@ -434,14 +434,37 @@ class DatabaseSearch:
     def topk(self, k: int = 100) -> torch.Tensor:
         """k best (score desc, global id asc) as int64 [k, 4] on the device."""
         o, d = self.out, self.dev
+        self.launches += 3  # sw_topk: histogram + threshold, compaction, one-CTA sort
         return topk_records(o["score"], d.ids, o["ref_end"], o["query_end"], k)
+
+
+_TOPK_WORK: dict = {}
 
 
 def topk_records(score: torch.Tensor, ids: torch.Tensor, ref_end: torch.Tensor,
                  query_end: torch.Tensor, k: int) -> torch.Tensor:
     """The k best records (score desc, global id asc) as int64 [k, 4]
-    (score, target_id, ref_end, query_end); works on any device."""
+    (score, target_id, ref_end, query_end).  Device tensors go through the library's
+    own top-k (``sw_topk``: score histogram -> threshold -> compaction -> one-CTA
+    sort); host tensors (the gloo tests) through torch."""
     k = min(k, int(score.shape[0]))
+    if (score.is_cuda and 1 <= k <= 1024 and score.dtype == torch.int32
+            and ids.dtype == torch.int64 and ref_end.dtype == torch.int32
+            and query_end.dtype == torch.int32):
+        L = _lib.load()
+        dev = score.device.index if score.device.index is not None else torch.cuda.current_device()
+        st = torch.cuda.current_stream()
+        wkey = (dev, st.cuda_stream)  # launches on one stream run in order: one scratch each
+        work = _TOPK_WORK.get(wkey)
+        if work is None:
+            work = torch.empty(int(L.sw_topk_workspace()), dtype=torch.uint8, device=score.device)
+            _TOPK_WORK[wkey] = work
+        rec = torch.empty((k, 4), dtype=torch.int64, device=score.device)
+        n = int(score.shape[0])
+        _lib.check(L.sw_topk(score.contiguous().data_ptr(), ids.contiguous().data_ptr(),
+                             ref_end.contiguous().data_ptr(), query_end.contiguous().data_ptr(),
+                             n, k, rec.data_ptr(), work.data_ptr(), st.cuda_stream))
+        return rec
     key = (score.to(torch.int64) << 32) | (0xFFFFFFFF - ids.to(torch.int64))
     _, idx = torch.topk(key, k, sorted=True)
     return torch.stack([score[idx].to(torch.int64), ids[idx].to(torch.int64),
