@@ -124,6 +124,20 @@ struct W16 {
 #endif
     }
   }
+  // the same with the source lane precomputed (kept in a register by the caller)
+  template <int T, int K>
+  __device__ static __forceinline__ uint32_t shift_from(uint32_t v, int src, uint32_t gmask, uint32_t sel) {
+    if constexpr (K == T) {
+      return v << 16;
+    } else {
+      uint32_t r = __shfl_sync(gmask, v, src, T);
+#if SWB_IMAD_SHIFT
+      return mul_lo(r, sel);
+#else
+      return prmt(r, 0u, sel);
+#endif
+    }
+  }
   __device__ static __forceinline__ uint32_t shift_sel(int t, int k) {
 #if SWB_IMAD_SHIFT
     return t >= k ? 1u : 0x10000u;
@@ -285,6 +299,9 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #ifndef SWB_IMM_DECAY
 #define SWB_IMM_DECAY 1
 #endif
+#ifndef SWB_PIN_SHIFT
+#define SWB_PIN_SHIFT 1
+#endif
 #ifndef SWB_PREF_D
 #define SWB_PREF_D 0  // residue prefetch distance in columns (segments of <= 32 words); 0: the unroll factor
 #endif
@@ -394,6 +411,22 @@ sw_striped_kernel(const SwArgs a) {
   uint32_t sel[6];
 #pragma unroll
   for (int s = 0; s < 6; ++s) sel[s] = Wd::shift_sel(t, 1 << s);
+
+  // Source lanes of the shifts.  With the exact kernels at the register limit ptxas
+  // rebuilt these and the selectors from SR_TID inside the column loop (S2R + in-order
+  // wait every iteration); pinned, they stay in registers.
+  int srcl[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) srcl[s] = (t - (1 << s)) & (T - 1);
+  constexpr bool kPinShift = SWB_PIN_SHIFT && Wd::LPW == 2 && EXACT;
+  if constexpr (kPinShift) {
+#pragma unroll
+    for (int s = 0; s < 6; ++s)
+      if ((1 << s) < T) asm volatile("" : "+r"(sel[s]), "+r"(srcl[s]));
+  }
+#define SWB_SHIFT(K, S, v, mask)                                                   \
+  (kPinShift ? W16::template shift_from<T, (K)>((v), srcl[S], (mask), sel[S])      \
+             : Wd::template shift<T, (K)>((v), t, (mask), sel[S]))
 
   // radix scan (T = 4): selectors of the shifts by 3, 5, 6 and 7 lanes (multipliers)
   const uint32_t rsel3 = t >= 3 ? 1u : 0x10000u;
@@ -702,7 +735,7 @@ sw_striped_kernel(const SwArgs a) {
       uint32_t w = H[LMAX - 1];
       if constexpr (FUSE3) w = Wd::vmax(Wd::vmax(Wd::add(carry, NWRAP), w), Fs[LMAX - 1]);
       else if constexpr (VAR == VAR_SCAN) w = Wd::addmax(carry, NWRAP, w);
-      uint32_t vh = Wd::template shift<T, 1>(w, t, cmask, sel[0]);
+      uint32_t vh = SWB_SHIFT(1, 0, w, cmask);
       uint32_t F = 0u;
       // fused words: carry - j*ge for the word being read, as kCjS interleaved running
       // adds (each value feeds a maximum and the next add, which keeps ptxas from folding
@@ -883,12 +916,11 @@ sw_striped_kernel(const SwArgs a) {
         const uint32_t u2 = Wd::addmax(s7, NKD[1], t3);
         carry = Wd::addmax_relu(u2, NKD[2], u1);
       } else if constexpr (VAR == VAR_SCAN) {
-        uint32_t acc = Wd::template shift<T, 1>(F, t, cmask, sel[0]);
+        uint32_t acc = SWB_SHIFT(1, 0, F, cmask);
         // Alg. 6 weighted max-scan, k = 1, 2, 4, ... (src/_compiled.py:320-336)
 #define SWB_STEP(S)                                                                         \
   if constexpr ((S) < STEPS) {                                                             \
-    acc = Wd::addmax_relu(Wd::template shift<T, (1 << (S))>(acc, t, cmask, sel[S]), NKD[S], \
-                          acc);                                                            \
+    acc = Wd::addmax_relu(SWB_SHIFT((1 << (S)), S, acc, cmask), NKD[S], acc);                \
   }
         SWB_STEP(0) SWB_STEP(1) SWB_STEP(2) SWB_STEP(3) SWB_STEP(4) SWB_STEP(5)
 #undef SWB_STEP
