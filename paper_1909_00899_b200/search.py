@@ -187,7 +187,7 @@ class DatabaseSearch:
     both modes. One launch, no host sync.
     """
 
-    SAMPLE_STRIDE = 16
+    SAMPLE_STRIDE = int(os.environ.get("SWB_SAMPLE_STRIDE", "16"))  # coordinate-floor sample: every n-th target
 
     def __init__(self, scheme: ScoringScheme, kernel: str = "scan", lanes: int = 0,
                  coords: str = "all", k: int = 100):
