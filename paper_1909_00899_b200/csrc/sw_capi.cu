@@ -527,16 +527,20 @@ int32_t sw_pairs_align(int32_t width, int32_t lanes, int32_t kernel, const uint8
   a.pass_stats = d_pass_stats;
   const bool vec = max_block == 128;  // exact instance: vectorised profile layout
   const int lslice = vec ? (p.seg_len + 3) / 4 * 4 : p.seg_len;
-  a.pair_stride = (n_sym + 1) * lslice * p.threads;
+  // exact instances: A rows per group slice + one shared null-residue row per CTA
+  const int rows = vec ? n_sym : n_sym + 1;
+  a.pair_stride = rows * lslice * p.threads;
   // block size: as many warps as the per-group profile slices allow (<= 256 threads)
   int block = max_block;
   // slice bytes / T, + the end-coordinate snapshot of the thread (SWB_SNAP)
   const int lmax_k = vec ? p.seg_len : p.lmax;
   const bool snap = SWB_SNAP && (d_ref_end || d_query_end);  // score-only: no snapshots
   const size_t per_thread =
-      (size_t)(n_sym + 1) * lslice * 4 + (snap ? (size_t)(lmax_k | 1) * 4 : 0);
+      (size_t)rows * lslice * 4 + (snap ? (size_t)(lmax_k | 1) * 4 : 0);
   while (block > 32 && per_thread * block > 110 * 1024) block >>= 1;
-  const size_t smem = per_thread * block + kPairSubWords * 4;  // + the staged matrix
+  // + the staged matrix, + the shared null row ([ceil(L/4)][32 or 4T] words)
+  const size_t null_bytes = vec ? (size_t)(lslice / 4) * (p.threads <= 4 ? 32 : p.threads * 4) * 4 : 0;
+  const size_t smem = per_thread * block + kPairSubWords * 4 + null_bytes;
   if (smem > 227 * 1024) return fail(SW_ENOTSUP, "pair profile slice too large (%zu B)", smem);
   const int G = 32 / p.threads;
   const int64_t tasks = d_n_jobs ? 0 : (n + G - 1) / G;

@@ -299,6 +299,9 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #ifndef SWB_IMM_DECAY
 #define SWB_IMM_DECAY 1
 #endif
+#ifndef SWB_MINB5_L
+#define SWB_MINB5_L 0  // exact instances up to this many words register-capped for 5 CTAs per SM (19: config 3 126.0 -> 132.4 ms, off)
+#endif
 #ifndef SWB_PIN_SHIFT
 #define SWB_PIN_SHIFT 1
 #endif
@@ -343,7 +346,8 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 
 template <class Wd, int T, int LMAX, int VAR, bool EXACT = false, int GE = 0>
 __global__ void __launch_bounds__(EXACT ? (LMAX > 32 ? SWB_EXACT_LONG_BLOCK : 128) : 256,
-                                  EXACT ? (LMAX > 32 ? SWB_EXACT_LONG_MINB : SWB_EXACT_MINB) : 1)
+                                  EXACT ? (LMAX > 32 ? SWB_EXACT_LONG_MINB
+                                                     : LMAX <= SWB_MINB5_L ? 5 : SWB_EXACT_MINB) : 1)
 sw_striped_kernel(const SwArgs a) {
   // GE > 0: gap-extend penalty known at compile time, so every decay constant
   // (j*ge, k*L*ge) is an immediate operand of VIADDMNMX instead of a register.
@@ -496,9 +500,23 @@ sw_striped_kernel(const SwArgs a) {
   // then each group owns a slice of (A+1)*LMAX*T words
   uint32_t* const pbase = smem + (a.mode == 1 ? kPairSubWords : 0);
   const int8_t* const subs = reinterpret_cast<const int8_t*>(smem);
-  if (a.mode == 1 && a.sub != nullptr) {
-    int8_t* dst = reinterpret_cast<int8_t*>(smem);
-    for (int w = threadIdx.x; w < A * A; w += blockDim.x) dst[w] = a.sub[w];
+  // Exact pairs-mode instances keep ONE null-residue row per CTA behind the slices
+  // (instead of one per group: 20 % less shared memory, a fifth CTA per SM for
+  // 150-residue reads).  A slice unit is A rows of LP4*BW words, so from unit u the
+  // shared row is row (units - u) * A: the thread's null symbol is that row index and
+  // the row address needs no select.
+  const int units = (int)(blockDim.x / T) / GRP;
+  const int unit = ((int)(threadIdx.x >> 5) * G + gw) / GRP;
+  if (a.mode == 1) {
+    if (a.sub != nullptr) {
+      int8_t* dst = reinterpret_cast<int8_t*>(smem);
+      for (int w = threadIdx.x; w < A * A; w += blockDim.x) dst[w] = a.sub[w];
+    }
+    if constexpr (VEC) {
+      uint32_t* nullrow = pbase + (size_t)units * GRP * (size_t)a.pair_stride;
+      for (int w = threadIdx.x; w < LP4 * BW; w += blockDim.x)
+        nullrow[w] = Wd::pack(Wd::NULLV, Wd::NULLV);
+    }
     __syncthreads();
   }
   uint32_t* gslice =
@@ -537,7 +555,7 @@ sw_striped_kernel(const SwArgs a) {
   constexpr int kNch = (LMAX + kCh - 1) / kCh;
   // end-coordinate snapshots: SNW words per thread after the profile / the slices
   const int prof_w = a.mode == 0 ? (VEC ? (A + 1) * LP4 * BW : (A + 1) * L * T)
-                                 : (int)(blockDim.x / T) * a.pair_stride;
+                                 : (int)(blockDim.x / T) * a.pair_stride + (VEC ? LP4 * BW : 0);
   uint32_t* const snap = pbase + (prof_w + 3) / 4 * 4 + threadIdx.x * SNW;
   (void)snap;
 
@@ -627,8 +645,8 @@ sw_striped_kernel(const SwArgs a) {
             cl |= c0 << (8 * k);
             ch |= c1 << (8 * k);
           }
-          for (int sym = 0; sym <= A; ++sym) {
-            const int8_t* srow = subs + (sym < A ? sym : 0) * A;
+          for (int sym = 0; sym < A; ++sym) {  // (the null row is shared, see above)
+            const int8_t* srow = subs + sym * A;
             uint32_t wv[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -637,8 +655,7 @@ sw_striped_kernel(const SwArgs a) {
               for (int h = 0; h < Wd::LPW; ++h) {
                 const int qs = (int)(((h ? ch : cl) >> (8 * k)) & 0xffu);
                 int sv;
-                if (sym == A) sv = Wd::NULLV;
-                else if (qs == 0xff) sv = -bias;  // reference pad: profile 0 == -bias (src/profile.py:60-63)
+                if (qs == 0xff) sv = -bias;  // reference pad: profile 0 == -bias (src/profile.py:60-63)
                 else sv = pp ? (qs == sym ? mt : mm) : (int)srow[qs & 31];
                 v[h] = sv;
               }
@@ -706,7 +723,7 @@ sw_striped_kernel(const SwArgs a) {
     uint32_t cmk[kNch];
 #pragma unroll
     for (int k = 0; k < kNch; ++k) cmk[k] = 0u;
-    const int nullsym = A;
+    const int nullsym = (VEC && a.mode == 1) ? (units - unit) * A : A;
     // residues are fetched kPref columns ahead (a byte queue in registers): with short
     // segments a column is shorter than an L2 round trip, and the profile row address
     // (sym * LT) stalled on the load issued one column earlier (long-scoreboard stalls)
