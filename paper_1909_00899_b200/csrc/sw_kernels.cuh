@@ -302,6 +302,9 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #ifndef SWB_MINB5_L
 #define SWB_MINB5_L 0  // exact instances up to this many words register-capped for 5 CTAs per SM (19: config 3 126.0 -> 132.4 ms, off)
 #endif
+#ifndef SWB_BF_SNAP
+#define SWB_BF_SNAP 0  // branch-free end-coordinate snapshots for segments of <= 32 words (config 3: coordinates 156.1 -> 150.6 ms but score-only 126.0 -> 127.3 ms: off)
+#endif
 #ifndef SWB_PIN_SHIFT
 #define SWB_PIN_SHIFT 1
 #endif
@@ -846,7 +849,21 @@ sw_striped_kernel(const SwArgs a) {
         }
         if (gate_open) {
         const int cmx = Wd::hmax(cm);
-        if (SNAP && cmx > gb) {
+        if constexpr (SNAP && SWB_BF_SNAP && LMAX <= 32 && Wd::LPW == 2) {
+          // short segments (pair batches): on planted reads some thread of the warp improves
+          // in almost every column, so the snapshot runs branch-free -- selects for the
+          // record and LMAX predicated stores instead of a divergent region
+          const int lo = Wd::get(cm, 0), hi = Wd::get(cm, 1);
+          const bool up = cmx > gb && cmx > bv;
+          bv = up ? cmx : bv;
+          bcol = up ? i : bcol;
+          bh = up ? (hi > lo ? 1 : 0) : bh;
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(snap);
+#pragma unroll
+          for (int c = 0; c < LMAX; ++c)
+            asm volatile("{.reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.b32 [%0], %1;}" ::"r"(sa + 4 * c),
+                         "r"(H[c]), "r"((uint32_t)up) : "memory");
+        } else if (SNAP && cmx > gb) {
           bool now = false;
 #pragma unroll
           for (int h = 0; h < Wd::LPW; ++h) {
