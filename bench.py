@@ -616,8 +616,8 @@ def device_config2(args, w, rank, world, timer, L):
                         f"{args.kernel.upper()},ge={w.scheme.gap_extend}>"),
         "width": 16, "alg_bytes": alg_bytes,
         # dram__bytes_read+write per launch of this kernel (one ncu --set full capture at
-        # this config, profiles/r01i_config2_db_kernel.md)
-        "traffic": 509.05e6,
+        # this config, profiles/r02f_config2_db_kernel.md: 499.69 MB read + 11.59 MB written)
+        "traffic": 511.28e6,
         "extra_config": {"lanes": eng.plan16.lanes, "seg_len": eng.plan16.seg_len,
                          "end_coords": "exact for every target scoring >= the in-kernel floor "
                                        "(k-th best of a strided 1/16 sample: a superset of the "
@@ -685,10 +685,10 @@ def device_config3(args, w, rank, world, timer, L):
         "rank_cells": 150 * 300 * n, "h2d": e2e_batch.h2d_bytes, "d2h": e2e_batch.d2h_bytes,
         "kernel_name": "sw_striped_kernel<W16,T=4,L=19,SCAN,exact,ge=1> (pairs mode, score-only)",
         "width": 16, "alg_bytes": alg_bytes,
-        # dram__bytes_read+write of this kernel: 507.88 MB per 2^20 pairs in one ncu
-        # --set full capture (profiles/r02k_config3_pairs_kernel_score.md), scaled to
+        # dram__bytes_read+write of this kernel: 508.01 MB per 2^20 pairs in one ncu
+        # --set full capture (profiles/r02f_config3_pairs_kernel_score.md), scaled to
         # the rank's pairs
-        "traffic": 507.88e6 * n / (1 << 20), "variants": variants,
+        "traffic": 508.01e6 * n / (1 << 20), "variants": variants,
         "extra_config": {"lanes": 8, "seg_len": 19},
         "result": lambda out: _gathered_pairs(out, n, args.n_pairs),
     }
