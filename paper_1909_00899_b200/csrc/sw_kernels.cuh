@@ -554,7 +554,7 @@ sw_striped_kernel(const SwArgs a) {
   constexpr bool SNAP = SWB_SNAP;
   constexpr int SNW = LMAX | 1;  // snapshot words per thread (odd: rows spread over the banks)
   // (chunked column maxima also with SNAP: independent accumulators, short chains)
-  constexpr int kCh = SWB_KCH > 0 ? SWB_KCH : (EXACT && LMAX > 32 ? 16 : 8);
+  constexpr int kCh = SWB_KCH > 0 ? SWB_KCH : (EXACT && LMAX > 32 ? 32 : 8);  // (config 2: 8 / 16 / 20 / 32 / 64 words per accumulator: 26.77 / 26.66 / 26.17 / 26.09 / 26.30 ms)
   constexpr int kNch = (LMAX + kCh - 1) / kCh;
   // end-coordinate snapshots: SNW words per thread after the profile / the slices
   const int prof_w = a.mode == 0 ? (VEC ? (A + 1) * LP4 * BW : (A + 1) * L * T)
