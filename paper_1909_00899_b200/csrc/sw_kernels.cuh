@@ -327,10 +327,10 @@ constexpr int kFloorBins = 4096;  // sample-score histogram bins (scores >= 4095
 #define SWB_FUSE3_MAXL 32  // longest segment using it (3 state words per query word)
 #endif
 #ifndef SWB_FUSE3_PARTIAL
-#define SWB_FUSE3_PARTIAL 30  // longer segments: the first N words use it (register budget)
+#define SWB_FUSE3_PARTIAL 38  // longer segments: the first N words use it (register budget)
 #endif
 #ifndef SWB_FUSE3_REGS
-#define SWB_FUSE3_REGS 146  // state-word budget (2 per word + 1 per fused word)
+#define SWB_FUSE3_REGS 156  // state-word budget (2 per word + 1 per fused word)
 #endif
 #ifndef SWB_FUSE3_PARTIAL_UNROLL
 #define SWB_FUSE3_PARTIAL_UNROLL 2
@@ -387,8 +387,10 @@ sw_striped_kernel(const SwArgs a) {
   // longer segments fuse only their first KF words: a fused word keeps three state
   // registers (u, entering F, E), so 2*LMAX + KF stays inside the register file
   // (measured on config 2, L = 58: 24 / 30 / 36 / 42 / 57 fused words -> 27.77 / 27.48 /
-  // 27.57 / 29.20 / 28.87 ms against 28.40 ms unfused)
-  constexpr int kFuseBudget = SWB_FUSE3_REGS - (T >= 16 ? 20 : 0) - 2 * LMAX;
+  // 27.57 / 29.20 / 28.87 ms against 28.40 ms unfused; with two max accumulators
+  // 30 / 34 / 36 / 38 / 40 -> 26.08 / 26.10 / 25.97 / 25.75 / 26.04 ms)
+  constexpr int kFuseBudget = SWB_FUSE3_REGS - (T >= 16 ? 20 : 0) - 2 * LMAX -
+                              (LMAX > 58 ? 2 * (LMAX - 58) + 4 : 0);  // (no spills up to 64 words)
   constexpr int kFuseWords = kFuseBudget < SWB_FUSE3_PARTIAL ? (kFuseBudget < 0 ? 0 : kFuseBudget) : SWB_FUSE3_PARTIAL;
   constexpr int KF = FUSE3 ? LMAX
                      : (SWB_FUSE3 && VAR == VAR_SCAN && EXACT && GE > 0) ? (kFuseWords < LMAX ? kFuseWords : LMAX - 1)
