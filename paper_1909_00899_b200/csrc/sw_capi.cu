@@ -42,6 +42,11 @@ KernelTable g_tab[2][3];
 ExactTable g_exact;  // 16-bit scan, exact segment length
 const void* g_chain[2][6];  // strip pipeline [width][L = 1, 2, 4, 8, 16, 32]
 const void* g_chain_so[6];  // 32-bit score-only strips [L]
+#ifndef SWB_CHAIN_GE1
+#define SWB_CHAIN_GE1 1  // 32-bit strips: instances with gap extend 1 as a compile-time constant
+#endif
+const void* g_chain_g1[6];     // 32-bit strips, gap extend 1 as a compile-time constant
+const void* g_chain_so_g1[6];
 const void* g_chain_prof[2];
 const void* g_wave[4][4];  // [L = 1, 2, 4, 8][KC = 1, 2, 4, 8]
 const void* g_block[2][3][16];  // block / cluster scan [width][variant][L-1]  // strip pipeline, intra-strip wavefront [L = 1, 2, 4, 8]
@@ -67,6 +72,7 @@ void init_tables() {
   // T = 2 (4 stripes): 33..40 words, pair batches of ~150-residue reads at lanes = 4
   swb_fill_exact_t2_g0_c(g_exact); swb_fill_exact_t2_g1_c(g_exact); swb_fill_exact_t2_g2_c(g_exact);
   swb_fill_chain(g_chain, g_chain_prof, g_chain_so);
+  swb_fill_chain_g1(g_chain_g1, g_chain_so_g1);
   swb_fill_wave(g_wave);
   swb_fill_block16(g_block[0]);
   swb_fill_block32(g_block[1]);
@@ -731,8 +737,11 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
   // score-only launches (no coordinate outputs) of the 32-bit strips skip the
   // end-coordinate tracking
   const bool score_only = !d_ref_end && !d_query_end;
+  const bool g1 = wi == 1 && gap_extend == 1 && SWB_CHAIN_GE1 && !getenv("SWB_CHAIN_NO_GE1");
   const void* fn = wave ? g_wave[g.li][g.ki]
-                        : (wi == 1 && score_only && SWB_CHAIN_SPLIT_SO ? g_chain_so[g.li] : g_chain[wi][g.li]);
+                        : (wi == 1 && score_only && SWB_CHAIN_SPLIT_SO
+                               ? (g1 ? g_chain_so_g1[g.li] : g_chain_so[g.li])
+                               : (g1 ? g_chain_g1[g.li] : g_chain[wi][g.li]));
   const size_t smem = wave ? (size_t)(n_sym + 1) * g.L * 32 * 4 + 128 * g.KC + 3 * kChainK * g.KC * 8  // residues, tile_in, 2 x tile_out
                            : (size_t)(n_sym + 1) * g.L * 32 * 4 + (kChainK + 1) * 16 + kChainK * 8
                                  + (width == 32 ? (size_t)(n_sym + 1) * 32 * 8 + 1024 : 0);  // + tile staging, (B, C) table, scan buffers

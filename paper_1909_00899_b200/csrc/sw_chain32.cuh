@@ -43,7 +43,10 @@
 
 namespace swb {
 
-template <int L, bool COORDS = true>
+// GE > 0: gap-extend penalty known at compile time, so the lane decays (d, 2d, .. 16d,
+// the wrap decay) and the E / F decay are immediate operands (fewer register sources
+// on the scan's critical path).
+template <int L, bool COORDS = true, int GE = 0>
 __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
   constexpr int T = 32;
   constexpr int RING = kChainRing * kChainK;
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(32) sw_chain32_kernel(const ChainArgs a) {
   for (int k = t; k < 256; k += 32) sbuf[k] = 0;
 
   const int CL = W32::CLAMP;
-  const int go = min(a.go, CL), ge = min(a.ge, CL);
+  const int go = min(a.go, CL), ge = GE > 0 ? GE : min(a.ge, CL);
   const int d = min(L * ge, CL);                       // decay per lane
   const int dw = (int)min((int64_t)(L - 1) * ge, (int64_t)CL);  // wrap decay
   const int kB = (int)min((int64_t)go + (int64_t)(L >= 2 ? L - 2 : 0) * ge, (int64_t)CL);
