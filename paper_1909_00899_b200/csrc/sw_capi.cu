@@ -49,6 +49,7 @@ const void* g_chain_g1[6];     // 32-bit strips, gap extend 1 as a compile-time 
 const void* g_chain_so_g1[6];
 const void* g_chain_prof[2];
 const void* g_wave[4][4];  // [L = 1, 2, 4, 8][KC = 1, 2, 4, 8]
+const void* g_wave_g1[4][4];  // the same with gap extend 1 as a compile-time constant
 const void* g_block[2][3][16];  // block / cluster scan [width][variant][L-1]  // strip pipeline, intra-strip wavefront [L = 1, 2, 4, 8]
 std::once_flag g_once;
 
@@ -74,6 +75,7 @@ void init_tables() {
   swb_fill_chain(g_chain, g_chain_prof, g_chain_so);
   swb_fill_chain_g1(g_chain_g1, g_chain_so_g1);
   swb_fill_wave(g_wave);
+  swb_fill_wave_g1(g_wave_g1);
   swb_fill_block16(g_block[0]);
   swb_fill_block32(g_block[1]);
   swb_fill_w16_scan(g_tab[0][VAR_SCAN]);
@@ -738,7 +740,8 @@ int32_t sw_align_long(int32_t width, int32_t kernel, const uint8_t* d_query, int
   // end-coordinate tracking
   const bool score_only = !d_ref_end && !d_query_end;
   const bool g1 = wi == 1 && gap_extend == 1 && SWB_CHAIN_GE1 && !getenv("SWB_CHAIN_NO_GE1");
-  const void* fn = wave ? g_wave[g.li][g.ki]
+  const void* fn = wave ? (gap_extend == 1 && SWB_CHAIN_GE1 && !getenv("SWB_CHAIN_NO_GE1") ? g_wave_g1[g.li][g.ki]
+                                                                                             : g_wave[g.li][g.ki])
                         : (wi == 1 && score_only && SWB_CHAIN_SPLIT_SO
                                ? (g1 ? g_chain_so_g1[g.li] : g_chain_so[g.li])
                                : (g1 ? g_chain_g1[g.li] : g_chain[wi][g.li]));

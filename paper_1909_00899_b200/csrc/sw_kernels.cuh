@@ -1208,5 +1208,6 @@ SWB_X_DECL(2, 0, c) SWB_X_DECL(2, 1, c) SWB_X_DECL(2, 2, c)
 void swb_fill_chain(const void* (&tab)[2][6], const void* (&ptab)[2], const void* (&so)[6]);
 void swb_fill_chain_g1(const void* (&tab)[6], const void* (&so)[6]);
 void swb_fill_wave(const void* (&tab)[4][4]);
+void swb_fill_wave_g1(const void* (&tab)[4][4]);
 void swb_fill_block16(const void* (&tab)[3][16]);
 void swb_fill_block32(const void* (&tab)[3][16]);

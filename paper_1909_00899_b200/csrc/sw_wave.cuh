@@ -169,7 +169,8 @@ __device__ __forceinline__ void wave_step(WaveLane<L, KC>& w, const int s, const
   }
 }
 
-template <int L, int KC>
+// GE > 0: gap-extend penalty known at compile time (decays as immediate operands)
+template <int L, int KC, int GE = 0>
 __global__ void __launch_bounds__(32) sw_wave_kernel(const ChainArgs a) {
   constexpr int TS = kChainK;        // steps (super-columns) per handoff tile
   constexpr int TC = TS * KC;        // columns per handoff tile
@@ -214,10 +215,11 @@ __global__ void __launch_bounds__(32) sw_wave_kernel(const ChainArgs a) {
   __syncwarp();
 
   const int cl = W32::CLAMP;
-  const uint32_t NGO = (uint32_t)-min(a.go, cl), NGE = (uint32_t)-min(a.ge, cl);
+  const int ge_ = GE > 0 ? GE : a.ge;
+  const uint32_t NGO = (uint32_t)-min(a.go, cl), NGE = (uint32_t)-min(ge_, cl);
   uint32_t NJG[L + 1];  // -j * ge (clamped): decay of the incoming F at row j
 #pragma unroll
-  for (int j = 0; j <= L; ++j) NJG[j] = (uint32_t)-(int)min((int64_t)j * a.ge, (int64_t)cl);
+  for (int j = 0; j <= L; ++j) NJG[j] = (uint32_t)-(int)min((int64_t)j * ge_, (int64_t)cl);
   WaveLane<L, KC> w;
 #pragma unroll
   for (int j = 0; j < L; ++j) { w.H[j] = 0u; w.E[j] = 0u; }
