@@ -96,3 +96,42 @@ def test_exact_instances_all_segment_lengths(A, oracle, lanes, ge):
         assert (so["score"].cpu().numpy() == sc).all(), (lanes, L, ge, "score-only")
         tried += 1
     assert tried >= 8, f"only {tried} segment lengths had an instance at {lanes} lanes"
+
+
+@pytest.mark.parametrize("ge", [1, 2, 3])
+def test_exact_pair_instances_uniform_queries_ragged_targets(A, oracle, ge):
+    """Pairs mode through the exact instances (uniform query length per batch, so every
+    pair has the same segment length) with targets of very different lengths inside one
+    warp: the short ones run on the shared null-residue row while their neighbours
+    finish.  Every segment length 1..32 at 8 stripes, scores and end coordinates
+    against the scalar oracle, with and without coordinate outputs."""
+    from paper_1909_00899_b200.scoring import ScoringScheme
+
+    rng = np.random.default_rng(0xA11CE + ge)
+    mat = np.full((4, 4), -3, dtype=np.int64)
+    np.fill_diagonal(mat, 2)
+    go = ge + 4
+    sch = ScoringScheme.from_array(mat, go, ge)
+    for L in range(1, 33):
+        m = 8 * L - int(rng.integers(0, 8))
+        m = max(m, 1)
+        n = 96
+        tl = rng.integers(1, 3 * m + 40, n)
+        tl[::7] = 1
+        q_off = (np.arange(n + 1) * m).astype(np.int64)
+        r_off = np.concatenate([[0], np.cumsum(tl)]).astype(np.int64)
+        fr = rng.integers(0, 4, r_off[-1]).astype(np.uint8)
+        fq = rng.integers(0, 4, q_off[-1]).astype(np.uint8)
+        for i in range(0, n, 2):  # plant a mutated piece of the target in the query
+            t = fr[r_off[i]:r_off[i + 1]]
+            k = min(len(t), m)
+            if k >= 4:
+                piece = t[:k].copy()
+                piece[rng.random(k) < 0.05] = rng.integers(0, 4)
+                fq[q_off[i] + m - k:q_off[i] + m] = piece
+        s, re_, qe = oracle.batch_scalar(fq, q_off, fr, r_off, sub=mat, go=go, ge=ge)
+        r = A.pairs_align(fq, q_off, fr, r_off, kernel="scan", scheme=sch)
+        assert (r["score"] == s).all(), (L, ge, "score")
+        assert (r["ref_end"] == re_).all() and (r["query_end"] == qe).all(), (L, ge, "coords")
+        so = A.pairs_align(fq, q_off, fr, r_off, kernel="scan", scheme=sch, coords=False)
+        assert (so["score"] == s).all(), (L, ge, "score-only")
