@@ -395,7 +395,10 @@ sw_striped_kernel(const SwArgs a) {
   constexpr int KF = FUSE3 ? LMAX
                      : (SWB_FUSE3 && VAR == VAR_SCAN && EXACT && GE > 0) ? (kFuseWords < LMAX ? kFuseWords : LMAX - 1)
                                                                          : 0;  // words in the fused form
-  constexpr int kColUnroll = FUSE3 ? SWB_FUSE3_UNROLL : KF > 0 ? SWB_FUSE3_PARTIAL_UNROLL
+  // (wide groups with short segments are the single-pair shapes, one warp's latency:
+  // config 1 at 16 stripes x 10 words runs 2.11 ms with two columns per iteration,
+  // 1.91 ms with one)
+  constexpr int kColUnroll = FUSE3 ? ((T >= 8 && LMAX <= 16) ? 1 : SWB_FUSE3_UNROLL) : KF > 0 ? SWB_FUSE3_PARTIAL_UNROLL
                                    : (EXACT && LMAX <= SWB_SHORT_L) ? SWB_COL_UNROLL_SHORT : SWB_COL_UNROLL;
 
   // a queue as deep as the unroll factor rotates by register renaming (no moves)
