@@ -203,6 +203,14 @@ int32_t sw_topk(const int32_t* d_score, const int64_t* d_ids, const int32_t* d_r
                 const int32_t* d_query_end, int64_t n, int32_t k, int64_t* d_records,
                 void* d_work, sw_stream_t stream);
 
+/* Expand 2-bit packed DNA (four residues per byte, residue k of a byte in bits
+ * 2k..2k+1) to one-byte codes on the device: d_codes[0 .. n_res).  The reference
+ * carries one code per element (Alphabet.encode, src/scoring.py:45-46); the packed
+ * form is an input format for host links that bound short-read batches.  d_codes
+ * 4-byte aligned for the fast path. */
+int32_t sw_unpack_2bit(const uint8_t* d_packed, int64_t n_res, uint8_t* d_codes,
+                       sw_stream_t stream);
+
 /* Device weighted max-plus scan over P lanes (reference weighted_max_scan /
  * _weighted_max_scan_c, src/kernels.py:177-201, src/_compiled.py:448-460):
  * d_f, d_out: uint16 [n][lanes]; d_d: decay per vector.  Values must fit the

@@ -35,6 +35,7 @@ EXPORTS = (
     "sw_collect_flagged",
     "sw_topk_workspace",
     "sw_topk",
+    "sw_unpack_2bit",
     "sw_scan_lanes",
     "sw_dpx_probe",
     "sw_long_workspace_bytes",
@@ -133,6 +134,8 @@ def load():
     L.sw_topk_workspace.argtypes = []
     L.sw_topk.restype = i32
     L.sw_topk.argtypes = [vp, vp, vp, vp, i64, i32, vp, vp, vp]
+    L.sw_unpack_2bit.restype = i32
+    L.sw_unpack_2bit.argtypes = [vp, i64, vp, vp]
     L.sw_scan_lanes.restype = i32
     L.sw_scan_lanes.argtypes = [i32, i32, vp, vp, i32, vp, vp]
     L.sw_dpx_probe.restype = i64

@@ -843,9 +843,17 @@ class PairsBatch:
         return self.out
 
     @staticmethod
-    def pin_host(flat_q, q_off, flat_r, r_off) -> dict:
-        """Pinned host copies of a CSR batch (the e2e input form)."""
+    def pin_host(flat_q, q_off, flat_r, r_off, packed2bit: bool = False) -> dict:
+        """Pinned host copies of a CSR batch (the e2e input form). ``packed2bit``: the
+        residues as four 2-bit codes per byte (``formats.pack_2bit``; DNA codes 0..3,
+        fixed-length batches), a quarter of the bytes over the host link; the device
+        expands each chunk (``sw_unpack_2bit``)."""
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        if packed2bit:
+            from .formats import pack_2bit
+
+            return {"q2": pin(pack_2bit(flat_q)), "q_off": np.asarray(q_off, np.int64),
+                    "t2": pin(pack_2bit(flat_r)), "r_off": np.asarray(r_off, np.int64)}
         return {"q": pin(np.asarray(flat_q, np.uint8)), "q_off": np.asarray(q_off, np.int64),
                 "t": pin(np.asarray(flat_r, np.uint8)), "r_off": np.asarray(r_off, np.int64)}
 
@@ -860,7 +868,13 @@ class PairsBatch:
         # follow from the two lengths, so they are generated on the device once instead of
         # being copied per chunk (the H2D carries residues only)
         self.uniform = n > 0 and bool((qlen == qlen[0]).all() and (tlen == tlen[0]).all())
+        self.packed2 = "q2" in host
         bounds = [n * c // n_chunks for c in range(n_chunks + 1)]
+        if self.packed2:
+            if not self.uniform:
+                raise ValueError("2-bit packed input needs a fixed-length batch")
+            # chunks start on a packed byte (and a 4-byte code word) of both streams
+            bounds = sorted({min(n, b // 32 * 32) for b in bounds[:-1]} | {n})
         chunks = []
         for a, b in zip(bounds[:-1], bounds[1:]):
             qs = q_off[a:b] - q_off[a]
@@ -875,8 +889,12 @@ class PairsBatch:
         mq = max(c[3] - c[2] for c in chunks)
         mt = max(c[5] - c[4] for c in chunks)
         mn = max(c[1] - c[0] for c in chunks)
-        self.bufs = [{"q": torch.empty(max(mq, 1), dtype=torch.uint8, device="cuda"),
-                      "t": torch.empty(max(mt, 1), dtype=torch.uint8, device="cuda"),
+        self.bufs = [{"q": torch.empty(max(mq, 1) + 16, dtype=torch.uint8, device="cuda"),
+                      "t": torch.empty(max(mt, 1) + 16, dtype=torch.uint8, device="cuda"),
+                      "q2": torch.empty((max(mq, 1) + 3) // 4 if self.packed2 else 1,
+                                        dtype=torch.uint8, device="cuda"),
+                      "t2": torch.empty((max(mt, 1) + 3) // 4 if self.packed2 else 1,
+                                        dtype=torch.uint8, device="cuda"),
                       "meta": torch.empty(6 * mn, dtype=torch.int32, device="cuda"),
                       "out": self._outputs(mn)} for _ in range(2)]
         self.host_out = {k: torch.empty(n, dtype=torch.int32).pin_memory()
@@ -888,8 +906,9 @@ class PairsBatch:
                           "ql": torch.full((mn,), int(qlen[0]), dtype=torch.int32, device="cuda"),
                           "tl": torch.full((mn,), int(tlen[0]), dtype=torch.int32, device="cuda")}
         self.copy_stream = torch.cuda.Stream()
-        self.h2d_bytes = int(host["q"].numel() + host["t"].numel()
-                             + sum(c[6].numel() * 4 for c in chunks if c[6] is not None))
+        self.h2d_bytes = int((host["q2"].numel() + host["t2"].numel()) if self.packed2 else
+                             (host["q"].numel() + host["t"].numel()
+                              + sum(c[6].numel() * 4 for c in chunks if c[6] is not None)))
         self.d2h_bytes = int(sum(v.numel() * v.element_size() for v in self.host_out.values()))
 
     def run_host(self, host: dict) -> dict:
@@ -906,10 +925,20 @@ class PairsBatch:
             with torch.cuda.stream(cp):
                 if c >= 2:
                     cp.wait_event(freed[c & 1])  # the chunk that used this buffer is done
-                buf["q"][: qb - qa].copy_(host["q"][qa:qb], non_blocking=True)
-                buf["t"][: tb - ta].copy_(host["t"][ta:tb], non_blocking=True)
+                if self.packed2:  # qa, ta are multiples of 4 (chunk bounds of 32 pairs)
+                    nq2, nt2 = (qb - qa + 3) // 4, (tb - ta + 3) // 4
+                    buf["q2"][:nq2].copy_(host["q2"][qa // 4:qa // 4 + nq2], non_blocking=True)
+                    buf["t2"][:nt2].copy_(host["t2"][ta // 4:ta // 4 + nt2], non_blocking=True)
+                else:
+                    buf["q"][: qb - qa].copy_(host["q"][qa:qb], non_blocking=True)
+                    buf["t"][: tb - ta].copy_(host["t"][ta:tb], non_blocking=True)
                 if meta is not None:
                     buf["meta"][: 6 * n].copy_(meta, non_blocking=True)
+                if self.packed2:  # expanded on the copy stream, beside the previous chunk's alignment
+                    L = _lib.load()
+                    _lib.check(L.sw_unpack_2bit(_ptr(buf["q2"]), qb - qa, _ptr(buf["q"]), cp.cuda_stream))
+                    _lib.check(L.sw_unpack_2bit(_ptr(buf["t2"]), tb - ta, _ptr(buf["t"]), cp.cuda_stream))
+                    self.launches += 2
                 ready[c].record(cp)
             cur.wait_event(ready[c])
             if meta is None:

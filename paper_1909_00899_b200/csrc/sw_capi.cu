@@ -847,6 +847,17 @@ int32_t sw_collect_flagged(const uint8_t* d_flags, int64_t n, uint8_t mask, int3
   return e == cudaSuccess ? SW_OK : cuda_fail(e, "sw_collect_kernel");
 }
 
+int32_t swb_unpack2_launch(const uint8_t* d_packed, int64_t n_res, uint8_t* d_codes,
+                           sw_stream_t stream);
+
+int32_t sw_unpack_2bit(const uint8_t* d_packed, int64_t n_res, uint8_t* d_codes,
+                       sw_stream_t stream) {
+  if (n_res < 0) return fail(SW_EINVAL, "n_res < 0");
+  if (n_res > 0 && (!d_packed || !d_codes)) return fail(SW_EINVAL, "NULL argument");
+  const int32_t rc = swb_unpack2_launch(d_packed, n_res, d_codes, stream);
+  return rc == 0 ? SW_OK : cuda_fail((cudaError_t)rc, "sw_unpack2_kernel");
+}
+
 int32_t swb_topk_launch(const int32_t* d_score, const int64_t* d_ids, const int32_t* d_ref_end,
                         const int32_t* d_query_end, int64_t n, int32_t k, int64_t* d_records,
                         void* d_work, sw_stream_t stream, const char** err);

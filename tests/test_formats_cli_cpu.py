@@ -222,3 +222,18 @@ def test_read_fasta_million_records_is_vectorised():
     assert (b.codes[: lens[0]] == lut[body[: lens[0]]]).all()
     assert (b.codes[-lens[-1]:] == lut[body[-lens[-1]:]]).all()
     assert dt < 20.0, dt
+
+
+def test_pack_2bit_roundtrip():
+    from paper_1909_00899_b200.formats import pack_2bit, unpack_2bit
+
+    rng = np.random.default_rng(5)
+    for n in (0, 1, 2, 3, 4, 5, 31, 32, 33, 4097):
+        c = rng.integers(0, 4, n).astype(np.uint8)
+        p = pack_2bit(c)
+        assert p.dtype == np.uint8 and p.size == (n + 3) // 4
+        assert (unpack_2bit(p, n) == c).all()
+    assert pack_2bit(np.array([1, 2, 3, 0, 3], np.uint8)).tolist() == [1 | 2 << 2 | 3 << 4, 3]
+    with pytest.raises(ValueError):
+        pack_2bit(np.array([0, 4], np.uint8))
+

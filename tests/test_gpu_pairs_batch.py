@@ -100,3 +100,46 @@ def test_database_search_four_stripes(A, oracle):
     assert (o["score"][: w.n_targets].cpu().numpy() == s[ids]).all()
     assert (o["ref_end"][: w.n_targets].cpu().numpy() == re_[ids]).all()
     assert (o["query_end"][: w.n_targets].cpu().numpy() == qe[ids]).all()
+
+
+def test_pairs_batch_2bit_packed_input(A, oracle):
+    """Fixed-length DNA batch from 2-bit packed pinned input (formats.pack_2bit, expanded on
+    the device by sw_unpack_2bit): same scores and coordinates as the one-byte input and the
+    oracle, a quarter of the H2D bytes; ragged batches are refused."""
+    import torch as T
+
+    from paper_1909_00899_b200 import workloads as W
+    from paper_1909_00899_b200.formats import pack_2bit, unpack_2bit
+
+    w = W.config3(n_pairs=5000)
+    sub = w.scheme.as_array()
+    s, re_, qe = oracle.batch_scalar(w.flat_q, w.q_off, w.flat_r, w.r_off, sub=sub,
+                                     go=w.scheme.gap_open, ge=w.scheme.gap_extend)
+    # the unpack kernel alone, odd lengths included
+    L = __import__("paper_1909_00899_b200._lib", fromlist=["load"]).load()
+    for n in (1, 3, 4, 5, 1023, 150 * 4999):
+        codes = np.ascontiguousarray(w.flat_q[:n])
+        d_p = T.from_numpy(pack_2bit(codes)).cuda()
+        d_c = T.full((n + 8,), 77, dtype=T.uint8, device="cuda")
+        assert L.sw_unpack_2bit(d_p.data_ptr(), n, d_c.data_ptr(), T.cuda.current_stream().cuda_stream) == 0
+        got = d_c.cpu().numpy()
+        assert (got[:n] == codes).all() and (got[n:] == 77).all(), n
+        assert (unpack_2bit(pack_2bit(codes), n) == codes).all()
+    for coords in (False, True):
+        b = A.PairsBatch(w.scheme, coords=coords)
+        host = b.pin_host(w.flat_q, w.q_off, w.flat_r, w.r_off, packed2bit=True)
+        b.prepare_host(host, n_chunks=7)
+        out = b.run_host(host)
+        T.cuda.synchronize()
+        assert b.h2d_bytes == (len(w.flat_q) + 3) // 4 + (len(w.flat_r) + 3) // 4
+        assert (out["score"].numpy() == s).all()
+        if coords:
+            assert (out["ref_end"].numpy() == re_).all() and (out["query_end"].numpy() == qe).all()
+    ragged = W.config3(n_pairs=64)
+    q_off = ragged.q_off.copy()
+    q_off[-1] -= 3
+    with pytest.raises(ValueError):
+        bb = A.PairsBatch(w.scheme)
+        bb.prepare_host(bb.pin_host(ragged.flat_q[:q_off[-1]], q_off, ragged.flat_r, ragged.r_off,
+                                    packed2bit=True), n_chunks=2)
+
